@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""Benchmark of the BD K/V projection (BASELINE.json metric) — one JSON line on rank 0.
+
+Workload (BASELINE config 2): DeepSeek-V2-Lite MLA kv_b_proj, kv_lora_rank d = 512,
+16 heads x (128 K_nope + 128 V), d_h = 128, FP16, 8192 tokens per GPU, random-init
+weights.  One step = the BD projection of K' AND V' (two problems, different tags, one
+kernel launch) for the step's tokens:
+
+    K' = X[:, S_k] + X[:, ~S_k] C_k,   V' = X[:, S_v] + X[:, ~S_v] C_v
+
+Arms
+  default            our kernel (libbd_kvproj.so via the package API), device-resident
+                     inputs -> `value`; the same call with pinned HOST buffers and the
+                     H2D/D2H copies inside the timed region -> `e2e`; cuBLAS dense
+                     projection with the original 512 x 4096 weight -> `baselines`.
+  --impl reference   the reference's CPU algorithm (the C oracle restatement; the
+                     reference is Python+numba and cannot travel to the GPU box) on all
+                     host threads, rank 0 only.
+
+Multi-GPU (torchrun): head-sharded weak scaling — rank r owns heads [r n/g, (r+1) n/g) of
+C_k and C_v and projects g x 8192 tokens, so per-GPU work is fixed and no collective sits
+on the data path; the step time is the max over ranks.
+
+L2 hygiene: the timed loop cycles through a ring of R buffer sets (x, C_k, C_v, K', V')
+whose total exceeds 2x the 126 MB L2, so no step finds its inputs in L2 from the
+previous use of the same buffers.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "BD K/V-proj tokens/s & speedup vs dense cuBLAS proj (DSV2-Lite FP16), 1-8 GPU"
+L2_BYTES = 126 * 2 ** 20
+
+CFG2 = dict(L=8192, d=512, d_h=128, n_heads=16)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--dtype", choices=["fp16", "bf16"], default="fp16")
+    ap.add_argument("--tokens", type=int, default=CFG2["L"], help="tokens per GPU per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["bf16_tflops"], d["hbm_gbs"], "measured"
+    return 1590.0, 6650.0, "fallback"  # B200_PROFILING.md fallback figures
+
+
+def load_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = ROOT / "profiles" / "latest_ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons through NVML while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.ok = False
+        self.samples: list[int] = []
+        self.reasons: set[str] = set()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            self.sample()
+            time.sleep(0.002)
+
+    def sample(self):
+        try:
+            self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+            r = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t is not None:
+            self._stop.set()
+            self._t.join()
+            self.sample()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": int(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def cpu_oracle_run(x16, ck16, cv16, d_h, n, threads):
+    """Reference algorithm (C restatement of attention.py:249-270) on float32 inputs,
+    K' and V' — the reference has no 16-bit path."""
+    from oracle import oracle as O
+    O.fused_kv_proj_ref(x16, ck16, d_h, n, "first", threads=threads)
+    O.fused_kv_proj_ref(x16, cv16, d_h, n, "last", threads=threads)
+
+
+def make_cpu_inputs(L, d, d_h, n):
+    import numpy as np
+    from oracle import oracle as O
+    rng = O.Rng(2024)
+    x = O.rand_gaussian(rng, L, d, np.float32)
+    ck = (O.rand_gaussian(rng, d - d_h, n * d_h, np.float32) / 8).astype(np.float32)
+    cv = (O.rand_gaussian(rng, d - d_h, n * d_h, np.float32) / 8).astype(np.float32)
+    return x, ck, cv
+
+
+def cpu_baseline(L, d, d_h, n, budget_s=12.0):
+    """Time the reference algorithm on the host: full-L steps until ~budget_s."""
+    from oracle import oracle as O
+    threads = O.default_threads()
+    x, ck, cv = make_cpu_inputs(L, d, d_h, n)
+    cpu_oracle_run(x[:64], ck, cv, d_h, n, threads)  # warm
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end or len(times) < 3:
+        t0 = time.perf_counter()
+        cpu_oracle_run(x, ck, cv, d_h, n, threads)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 50:
+            break
+    med = statistics.median(times)
+    return {"value": L / med, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"{len(times)} full steps of cfg2 K'+V' (L={L}, FP32, C restatement of "
+                      f"ref attention.py:249-270), median {med * 1e3:.1f} ms/step"}
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    d, d_h, n = CFG2["d"], CFG2["d_h"], CFG2["n_heads"]
+    L = args.tokens * world  # same whole-job tokens per step as our arm
+    threads = O.default_threads()
+    x, ck, cv = make_cpu_inputs(L, d, d_h, n)
+    # each step is a bounded sample of the step's tokens, scaled to the full step:
+    # the kernel is independent 8-row blocks (attention.py:254-257), linear in L.
+    sample_L = min(L, 8192)
+    for _ in range(args.warmup):
+        cpu_oracle_run(x[:sample_L], ck, cv, d_h, n, threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_oracle_run(x[:sample_L], ck, cv, d_h, n, threads)
+        times.append(time.perf_counter() - t0)
+    total = sum(times) * (L / sample_L)
+    value = args.steps * L / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": {"workload": "cfg2 DSV2-Lite kv_b_proj K'+V' (d=512, d_h=128, 16+16 heads)",
+                   "tokens_per_step": L, "sample_tokens_per_step": sample_L},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample_L} of {L} tokens per step, scaled by L/sample "
+                                   "(work is linear in L)"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_01718_b200 as bd
+    from paper_2510_01718_b200 import _native as N
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dtype = torch.float16 if args.dtype == "fp16" else torch.bfloat16
+    d, d_h, n_total = CFG2["d"], CFG2["d_h"], CFG2["n_heads"]
+    if n_total % world:
+        raise SystemExit(f"{n_total} heads do not shard over {world} GPUs")
+    n = n_total // world              # heads of K (and of V) owned by this rank
+    L = args.tokens * world           # head-sharded weak scaling: tokens grow with g
+    K = d - d_h
+    N_cols = n * d_h
+
+    # ring of buffer sets exceeding 2x L2
+    set_bytes = 2 * (L * d + 2 * K * N_cols + 2 * L * N_cols)
+    R = max(2, math.ceil(2 * L2_BYTES / set_bytes) + 1)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    xs = [torch.randn(L, d, device=dev, generator=g).to(dtype) for _ in range(R)]
+    cks = [(torch.randn(K, N_cols, device=dev, generator=g) / 8).to(dtype) for _ in range(R)]
+    cvs = [(torch.randn(K, N_cols, device=dev, generator=g) / 8).to(dtype) for _ in range(R)]
+    kos = [torch.empty(L, N_cols, device=dev, dtype=dtype) for _ in range(R)]
+    vos = [torch.empty(L, N_cols, device=dev, dtype=dtype) for _ in range(R)]
+    # dense comparator: original kv_b_proj weight (d x 2 N), one cuBLAS GEMM per step
+    ws = [(torch.randn(d, 2 * N_cols, device=dev, generator=g) / 8).to(dtype) for _ in range(R)]
+    dos = [torch.empty(L, 2 * N_cols, device=dev, dtype=dtype) for _ in range(R)]
+
+    def bd_step(i):
+        j = i % R
+        bd.fused_kv_proj_grouped(xs[j], [(cks[j], d_h, n, bd.Tag.FIRST),
+                                         (cvs[j], d_h, n, bd.Tag.LAST)],
+                                 outs=[kos[j], vos[j]])
+
+    def dense_step(i):
+        j = i % R
+        torch.matmul(xs[j], ws[j], out=dos[j])
+
+    stream = torch.cuda.Stream(device=dev)
+
+    def capture(step_fn, k):
+        for i in range(3):  # warm the path (attributes, cuBLAS handles) outside capture
+            step_fn(i)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        before = N.launch_count()
+        with torch.cuda.graph(graph, stream=stream):
+            for i in range(k):
+                step_fn(i)
+        return graph, N.launch_count() - before
+
+    def timed(graph_w, graph_t):
+        graph_w.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            s.record(stream)
+            graph_t.replay()
+            e.record(stream)
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    # dense cuBLAS comparator first (also settles clocks)
+    gdw, _ = capture(dense_step, args.warmup)
+    gdt, _ = capture(dense_step, args.steps)
+    dense_ms = timed(gdw, gdt)
+
+    gbw, _ = capture(bd_step, args.warmup)
+    gbt, launches = capture(bd_step, args.steps)
+    sampler = ClockSampler(local)
+    sampler.start()
+    bd_ms = timed(gbw, gbt)
+    sampler.stop()
+    # second measurement of the kernel alone for the roofline (same graph)
+    bd_ms2 = timed(gbw, gbt)
+    kern_ms = min(bd_ms, bd_ms2) / args.steps
+
+    ms_per_step = bd_ms / args.steps
+    # L already counts every rank's tokens: each rank projects all L tokens for its heads
+    value = L / (ms_per_step * 1e-3)
+    dense_value = L / (dense_ms / args.steps * 1e-3)
+
+    flops = 2 * 2 * L * K * N_cols  # K' and V', this rank (multiply FLOPs)
+    bytes_alg = 2 * (L * d + 2 * K * N_cols + 2 * L * N_cols)
+    peak_tf, peak_hbm, peak_kind = load_peaks()
+    achieved_tf = flops / (kern_ms * 1e-3) / 1e12
+    traffic = load_traffic()
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, bd, torch, dist, dev, world, dtype, L, d, d_h, n, cks[0], cvs[0])
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(L, d, d_h, n)
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": args.dtype,
+        "data": "synthetic (N(0,1) activations, random-init C_k/C_v and dense weight)",
+        "config": {
+            "workload": "cfg2: DSV2-Lite MLA kv_b_proj K'+V' (d=kv_lora_rank 512, d_h=128, "
+                        "16 K heads + 16 V heads, K tag FIRST, V tag LAST), one launch/step",
+            "tokens_per_step": L, "d": d, "d_h": d_h, "heads_per_gpu": n,
+            "parallelism": f"head-sharded x{world}" if world > 1 else "single GPU",
+            "l2": f"ring of {R} buffer sets, {R * set_bytes / 2**20:.0f} MiB > 2x126 MiB L2",
+        },
+        "roofline": {
+            "bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": achieved_tf / peak_tf, "traffic": traffic,
+            "peak_kind": f"{peak_kind} burst bf16/fp16 dense",
+            "kernel_us": kern_ms * 1e3,
+            "hbm_gbs": bytes_alg / (kern_ms * 1e-3) / 1e9, "hbm_peak_gbs": peak_hbm,
+            "algorithmic_bytes": bytes_alg, "algorithmic_flops": flops,
+        },
+        "baselines": {
+            "dense_cublas": {"value": dense_value, "unit": "tokens/s",
+                             "ms_per_step": dense_ms / args.steps,
+                             "what": "torch.matmul(x, W_kvb 512x4096) FP16, same ring"},
+            "speedup_vs_dense_cublas": value / dense_value,
+            "flop_ratio": d / (d - d_h),
+        },
+        "gpu_launches": launches,
+        "clocks": sampler.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, bd, torch, dist, dev, world, dtype, L, d, d_h, n, ck, cv):
+    """Same metric through the public API with pinned HOST buffers: every step copies its
+    x in (H2D), runs the grouped projection, and reads K', V' back (D2H)."""
+    N_cols = n * d_h
+    x_host = [torch.randn(L, d).to(dtype).pin_memory() for _ in range(2)]
+    k_host = [torch.empty(L, N_cols, dtype=dtype).pin_memory() for _ in range(2)]
+    v_host = [torch.empty(L, N_cols, dtype=dtype).pin_memory() for _ in range(2)]
+    specs = [(ck, d_h, n, bd.Tag.FIRST), (cv, d_h, n, bd.Tag.LAST)]
+    steps = max(3, min(args.steps, 50))
+
+    def step(i):
+        bd.fused_kv_proj_grouped_host(x_host[i % 2], specs, outs=[k_host[i % 2], v_host[i % 2]])
+
+    for i in range(3):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for i in range(steps):
+        step(i)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    esz = 2
+    return {"value": L / (ms / steps * 1e-3), "unit": "tokens/s",
+            "h2d_bytes_per_step": L * d * esz, "d2h_bytes_per_step": 2 * L * N_cols * esz,
+            "steps": steps, "api": "fused_kv_proj_grouped_host (pinned host x -> K', V')"}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,126 @@
+/*
+ * bd_kv_proj.h — C ABI of the B200-native basis-decomposed K/V projection.
+ *
+ * The projection (BD Attention, arXiv 2510.01718) is
+ *
+ *     out[i, h*d_h + j] = ( sum_{k=0}^{d-d_h-1} x[i, mul_base + k] * c[k, h*d_h + j] )
+ *                         + x[i, rep_base + j]
+ *
+ * for rows i < L, heads h < n_heads, j < d_h.  The tag of the reference picks the
+ * two offsets: FIRST -> (mul_base, rep_base) = (d_h, 0), LAST -> (0, d - d_h).
+ *
+ * Reference interface this replaces:
+ *   - bdattn.attention._fused_kernel(x, c, d_h, n_heads, mul_base, rep_base, out)
+ *       ref: pkg/src/bdattn/attention.py:249-270   (the numba "FFI" the Python op calls)
+ *   - bdattn.fused_kv_proj(x, c, d_h, n_heads, tag)
+ *       ref: pkg/src/bdattn/attention.py:273-295   (validation + tag -> offsets + allocation)
+ *
+ * Differences from the reference kernel that a binding author must know:
+ *   - every element of `out` is written exactly once (no pre-zeroed buffer needed;
+ *     the reference accumulates into a caller-zeroed array, attention.py:293-294,
+ *     which gives the same values because it starts from +0.0);
+ *   - device entry points are stream-ordered and asynchronous; *_host entry points
+ *     are synchronous and take host pointers, like the numba dispatcher call;
+ *   - FP32/FP64 run the "exact" kernel: per element, k ascending, one rounded
+ *     multiply then one rounded add per step (no FMA), then + the repeated slice —
+ *     the reference's rounding sequence (attention.py:258-265), hence bit-identical;
+ *   - FP16/BF16 run the tensor-core kernel (TMA -> tcgen05.mma -> TMEM, FP32
+ *     accumulate, gather-add of x[:, rep] in FP32 in the epilogue, one output
+ *     rounding).  The reference has no 16-bit path (ref: SPEC.md:138).
+ *
+ * All sizes are in elements; leading dimensions (ld*) are row strides in elements.
+ * Return value: BD_OK or one of BD_ERR_*; bd_last_error() describes the last failure
+ * on the calling thread.
+ */
+#ifndef BD_KV_PROJ_H
+#define BD_KV_PROJ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BD_KV_PROJ_ABI_VERSION 1
+
+/* element types */
+enum bd_dtype { BD_F32 = 0, BD_F64 = 1, BD_F16 = 2, BD_BF16 = 3 };
+
+/* status codes */
+enum bd_status {
+  BD_OK = 0,
+  BD_ERR_SHAPE = 1,  /* ref ShapeError (errors.py:4) */
+  BD_ERR_DTYPE = 2,  /* ref PrecisionError (errors.py:8) / unsupported dtype */
+  BD_ERR_ALIGN = 3,  /* tensor-core path needs 16-byte aligned rows/offsets */
+  BD_ERR_CUDA = 4,   /* a CUDA runtime/driver call failed */
+  BD_ERR_ARG = 5     /* null pointer, negative size, bad enum */
+};
+
+/* kernel selection */
+enum bd_mode {
+  BD_MODE_AUTO = 0,   /* F32/F64 -> exact, F16/BF16 -> tensor core */
+  BD_MODE_EXACT = 1,  /* SIMT, reference rounding order (F32/F64 only) */
+  BD_MODE_TC = 2      /* tcgen05 tensor cores (F16/BF16 only) */
+};
+
+/* tags (ref: decompose.py:27-31) */
+enum bd_tag { BD_TAG_FIRST = 0, BD_TAG_LAST = 1 };
+
+/* One projection problem. Pointers are device pointers for the device entry points. */
+typedef struct bd_kv_problem {
+  const void* x;    /* L x d,            row stride ldx */
+  const void* c;    /* (d - d_h) x N,    row stride ldc, N = n_heads * d_h */
+  void* out;        /* L x N,            row stride ldo */
+  int64_t ldx, ldc, ldo;
+  int64_t L, d, d_h, n_heads;
+  int64_t mul_base; /* first column of x multiplied by c  (FIRST: d_h, LAST: 0)     */
+  int64_t rep_base; /* first column of x repeated per head (FIRST: 0, LAST: d - d_h) */
+} bd_kv_problem;
+
+/*
+ * Fused K/V projection on device buffers, enqueued on `stream` (a cudaStream_t,
+ * NULL = legacy default stream).  `nonfinite_flag`, if not NULL, is a device int
+ * that the kernel sets to 1 when any output element is NaN/Inf (the reference
+ * raises ValueError for that, tensor.py:112-113); it is never cleared by the call.
+ * Replaces: _fused_kernel(x, c, d_h, n_heads, mul_base, rep_base, out)
+ *           (ref: pkg/src/bdattn/attention.py:249-270, called at :294).
+ */
+int bd_kv_proj(const void* x, int64_t ldx, const void* c, int64_t ldc, void* out, int64_t ldo,
+               int64_t L, int64_t d, int64_t d_h, int64_t n_heads, int64_t mul_base,
+               int64_t rep_base, int dtype, int mode, int* nonfinite_flag, void* stream);
+
+/*
+ * Several projections in ONE launch (bda_forward's K' and V', ref attention.py:305-306,
+ * or the K and V halves of an MLA kv_b_proj).  All problems share dtype and mode.
+ * count must be in [1, BD_MAX_GROUP].
+ */
+#define BD_MAX_GROUP 4
+int bd_kv_proj_grouped(const bd_kv_problem* problems, int count, int dtype, int mode,
+                       int* nonfinite_flag, void* stream);
+
+/*
+ * Synchronous host-buffer variant: x, c, out are HOST pointers (C-contiguous,
+ * ldx = d, ldc = ldo = N).  Copies in, runs the kernel on an internal stream,
+ * copies out, synchronises, and returns BD_ERR_CUDA... or BD_OK.  If *nonfinite
+ * is not NULL it receives 1 when the output holds NaN/Inf.  This is the entry a
+ * ctypes/numba-level drop-in for _fused_kernel binds.
+ * Device staging buffers are cached per thread and grown on demand.
+ */
+int bd_kv_proj_host(const void* x, const void* c, void* out, int64_t L, int64_t d, int64_t d_h,
+                    int64_t n_heads, int64_t mul_base, int64_t rep_base, int dtype, int mode,
+                    int* nonfinite);
+
+/* Human-readable description of the last error on this thread ("" if none). */
+const char* bd_last_error(void);
+
+/* BD_KV_PROJ_ABI_VERSION of the loaded library. */
+int bd_abi_version(void);
+
+/* Number of kernel launches issued by this library since load (all threads). */
+uint64_t bd_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BD_KV_PROJ_H */

@@ -1,0 +1,238 @@
+// capi.cu — the C ABI (include/bd_kv_proj.h): validation, kernel dispatch, the
+// synchronous host-buffer entry point and error reporting.
+//
+// Validation mirrors what the reference checks before it calls its kernel
+// (ref: pkg/src/bdattn/attention.py:283-288: precision first, then c's rows, then
+// c's cols) plus what a raw-pointer ABI needs (null pointers, strides, offsets,
+// 16-byte alignment for the TMA path).  Nothing is launched when a check fails.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/bd_kv_proj.h"
+#include "kv_proj_internal.h"
+
+namespace bdk {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+size_t elem_size(int dtype) {
+  switch (dtype) {
+    case BD_F32: return 4;
+    case BD_F64: return 8;
+    case BD_F16: return 2;
+    case BD_BF16: return 2;
+    default: return 0;
+  }
+}
+
+int resolve_mode(int dtype, int mode, int* out_mode) {
+  if (mode == BD_MODE_AUTO) {
+    *out_mode = (dtype == BD_F32 || dtype == BD_F64) ? BD_MODE_EXACT : BD_MODE_TC;
+    return BD_OK;
+  }
+  if (mode == BD_MODE_EXACT) {
+    if (dtype != BD_F32 && dtype != BD_F64)
+      return fail(BD_ERR_DTYPE, "exact mode supports F32/F64 only");
+    *out_mode = mode;
+    return BD_OK;
+  }
+  if (mode == BD_MODE_TC) {
+    if (dtype != BD_F16 && dtype != BD_BF16)
+      return fail(BD_ERR_DTYPE, "tensor-core mode supports F16/BF16 only");
+    *out_mode = mode;
+    return BD_OK;
+  }
+  return fail(BD_ERR_ARG, "unknown mode " + std::to_string(mode));
+}
+
+int validate(const bd_kv_problem& p, int dtype, int mode, int idx) {
+  char buf[256];
+  const std::string at = "problem " + std::to_string(idx) + ": ";
+  if (p.x == nullptr || p.c == nullptr || p.out == nullptr)
+    return fail(BD_ERR_ARG, at + "null pointer");
+  if (p.L < 1 || p.d < 2 || p.d_h < 1 || p.n_heads < 1) {
+    snprintf(buf, sizeof(buf), "non-positive size (L=%lld d=%lld d_h=%lld n_heads=%lld)",
+             (long long)p.L, (long long)p.d, (long long)p.d_h, (long long)p.n_heads);
+    return fail(BD_ERR_SHAPE, at + buf);
+  }
+  if (p.d_h >= p.d) {
+    snprintf(buf, sizeof(buf), "d_h (%lld) must be < d (%lld)", (long long)p.d_h,
+             (long long)p.d);
+    return fail(BD_ERR_SHAPE, at + buf);
+  }
+  const int64_t K = p.d - p.d_h;
+  const int64_t N = p.n_heads * p.d_h;
+  if (p.mul_base < 0 || p.mul_base + K > p.d || p.rep_base < 0 || p.rep_base + p.d_h > p.d) {
+    snprintf(buf, sizeof(buf), "offsets out of range (mul_base=%lld rep_base=%lld d=%lld d_h=%lld)",
+             (long long)p.mul_base, (long long)p.rep_base, (long long)p.d, (long long)p.d_h);
+    return fail(BD_ERR_SHAPE, at + buf);
+  }
+  if (p.ldx < p.d || p.ldc < N || p.ldo < N) {
+    snprintf(buf, sizeof(buf), "row strides too small (ldx=%lld ldc=%lld ldo=%lld, d=%lld N=%lld)",
+             (long long)p.ldx, (long long)p.ldc, (long long)p.ldo, (long long)p.d, (long long)N);
+    return fail(BD_ERR_SHAPE, at + buf);
+  }
+  if (p.L > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
+    return fail(BD_ERR_SHAPE, at + "dimension exceeds int32 range");
+  if (mode == BD_MODE_TC) {
+    if (!aligned16(p.x) || !aligned16(p.c) || !aligned16(p.out))
+      return fail(BD_ERR_ALIGN, at + "tensor-core path needs 16-byte aligned x, c and out");
+    if ((p.ldx | p.ldc | p.ldo | p.mul_base | p.rep_base | p.d_h) & 7) {
+      snprintf(buf, sizeof(buf),
+               "tensor-core path needs ldx, ldc, ldo, mul_base, rep_base and d_h to be multiples "
+               "of 8 (got %lld %lld %lld %lld %lld %lld)",
+               (long long)p.ldx, (long long)p.ldc, (long long)p.ldo, (long long)p.mul_base,
+               (long long)p.rep_base, (long long)p.d_h);
+      return fail(BD_ERR_ALIGN, at + buf);
+    }
+  }
+  (void)dtype;
+  return BD_OK;
+}
+
+int run_group(const bd_kv_problem* probs, int count, int dtype, int mode, int* flag,
+              cudaStream_t stream) {
+  if (probs == nullptr || count < 1 || count > BD_MAX_GROUP)
+    return fail(BD_ERR_ARG, "problem count must be in [1, " + std::to_string(BD_MAX_GROUP) + "]");
+  if (elem_size(dtype) == 0) return fail(BD_ERR_DTYPE, "unknown dtype " + std::to_string(dtype));
+  int m = 0;
+  int rc = resolve_mode(dtype, mode, &m);
+  if (rc != BD_OK) return rc;
+  for (int i = 0; i < count; ++i) {
+    rc = validate(probs[i], dtype, m, i);
+    if (rc != BD_OK) return rc;
+  }
+  g_last_error.clear();
+  if (m == BD_MODE_EXACT) {
+    cudaError_t e = launch_exact(probs, count, dtype, flag, stream);
+    if (e != cudaSuccess) return fail(BD_ERR_CUDA, std::string("kv_proj_exact: ") + cudaGetErrorString(e));
+    return BD_OK;
+  }
+  return launch_tc(probs, count, dtype, flag, stream);
+}
+
+// Per-thread device staging for the synchronous host entry point.
+struct HostStaging {
+  void* buf = nullptr;
+  size_t cap = 0;
+  int* flag = nullptr;
+  cudaStream_t stream = nullptr;
+  ~HostStaging() {
+    // Process teardown may already have destroyed the context; ignore errors.
+    if (buf) cudaFree(buf);
+    if (flag) cudaFree(flag);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+thread_local HostStaging g_staging;
+
+size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int sm_count() {
+  static int cached_dev = -1;
+  static int cached = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached = n > 0 ? n : 148;
+    cached_dev = dev;
+  }
+  return cached;
+}
+
+}  // namespace bdk
+
+extern "C" {
+
+int bd_kv_proj(const void* x, int64_t ldx, const void* c, int64_t ldc, void* out, int64_t ldo,
+               int64_t L, int64_t d, int64_t d_h, int64_t n_heads, int64_t mul_base,
+               int64_t rep_base, int dtype, int mode, int* nonfinite_flag, void* stream) {
+  bd_kv_problem p{x, c, out, ldx, ldc, ldo, L, d, d_h, n_heads, mul_base, rep_base};
+  return bdk::run_group(&p, 1, dtype, mode, nonfinite_flag, static_cast<cudaStream_t>(stream));
+}
+
+int bd_kv_proj_grouped(const bd_kv_problem* problems, int count, int dtype, int mode,
+                       int* nonfinite_flag, void* stream) {
+  return bdk::run_group(problems, count, dtype, mode, nonfinite_flag,
+                        static_cast<cudaStream_t>(stream));
+}
+
+int bd_kv_proj_host(const void* x, const void* c, void* out, int64_t L, int64_t d, int64_t d_h,
+                    int64_t n_heads, int64_t mul_base, int64_t rep_base, int dtype, int mode,
+                    int* nonfinite) {
+  using namespace bdk;
+  const size_t es = elem_size(dtype);
+  if (es == 0) return fail(BD_ERR_DTYPE, "unknown dtype " + std::to_string(dtype));
+  if (x == nullptr || c == nullptr || out == nullptr) return fail(BD_ERR_ARG, "null pointer");
+  if (L < 1 || d < 2 || d_h < 1 || n_heads < 1 || d_h >= d)
+    return fail(BD_ERR_SHAPE, "invalid sizes");
+  const int64_t K = d - d_h;
+  const int64_t N = n_heads * d_h;
+  const size_t bx = round_up(static_cast<size_t>(L * d) * es, 256);
+  const size_t bc = round_up(static_cast<size_t>(K * N) * es, 256);
+  const size_t bo = round_up(static_cast<size_t>(L * N) * es, 256);
+  HostStaging& s = g_staging;
+  cudaError_t e = cudaSuccess;
+  if (s.stream == nullptr) {
+    e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&s.flag, sizeof(int));
+    if (e != cudaSuccess) return fail(BD_ERR_CUDA, std::string("staging init: ") + cudaGetErrorString(e));
+  }
+  if (s.cap < bx + bc + bo) {
+    if (s.buf) cudaFree(s.buf);
+    s.buf = nullptr;
+    s.cap = 0;
+    e = cudaMalloc(&s.buf, bx + bc + bo);
+    if (e != cudaSuccess) return fail(BD_ERR_CUDA, std::string("staging alloc: ") + cudaGetErrorString(e));
+    s.cap = bx + bc + bo;
+  }
+  char* dx = static_cast<char*>(s.buf);
+  char* dc = dx + bx;
+  char* dout = dc + bc;
+  e = cudaMemsetAsync(s.flag, 0, sizeof(int), s.stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dx, x, static_cast<size_t>(L * d) * es, cudaMemcpyHostToDevice, s.stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dc, c, static_cast<size_t>(K * N) * es, cudaMemcpyHostToDevice, s.stream);
+  if (e != cudaSuccess) return fail(BD_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e));
+  bd_kv_problem p{dx, dc, dout, d, N, N, L, d, d_h, n_heads, mul_base, rep_base};
+  int rc = run_group(&p, 1, dtype, mode, s.flag, s.stream);
+  if (rc != BD_OK) {
+    cudaStreamSynchronize(s.stream);
+    return rc;
+  }
+  int hflag = 0;
+  e = cudaMemcpyAsync(out, dout, static_cast<size_t>(L * N) * es, cudaMemcpyDeviceToHost, s.stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hflag, s.flag, sizeof(int), cudaMemcpyDeviceToHost, s.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s.stream);
+  if (e != cudaSuccess) return fail(BD_ERR_CUDA, std::string("D2H: ") + cudaGetErrorString(e));
+  if (nonfinite) *nonfinite = hflag;
+  return BD_OK;
+}
+
+const char* bd_last_error(void) { return bdk::g_last_error.c_str(); }
+
+int bd_abi_version(void) { return BD_KV_PROJ_ABI_VERSION; }
+
+uint64_t bd_launch_count(void) { return bdk::g_launches.load(std::memory_order_relaxed); }
+
+}  // extern "C"

@@ -1,0 +1,158 @@
+// kv_proj_exact.cu — FP32/FP64 BD K/V projection in the reference's exact rounding order.
+//
+// The reference kernel (ref: pkg/src/bdattn/attention.py:249-270) computes, per output
+// element, acc = 0; for k ascending: acc = fl(acc + fl(x[i, mul_base+k] * c[k, j]));
+// then out = fl(acc + x[i, rep_base + j % d_h]).  numba compiles it without fast-math,
+// so no FMA contraction happens.  This kernel reproduces that sequence with
+// __fmul_rn/__fadd_rn (never contracted), so its output is bit-identical to the
+// reference for every shape — including the tiny odd shapes of the reference tests
+// (d=13, d_h=4, n=3; test_attention.py:187-203) that the tensor-core path cannot take.
+//
+// Tiling is for data reuse only: a 64x64 output tile per 256-thread CTA, k-slabs of
+// 16 staged through shared memory, 4x4 outputs per thread.  The per-element
+// reduction order is untouched by the tiling, which is also why column-sharding the
+// output across GPUs is bit-invariant (ref test_tensor.py:113-119).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kv_proj_internal.h"
+
+namespace bdk {
+namespace {
+
+constexpr int EX_BM = 64;
+constexpr int EX_BN = 64;
+constexpr int EX_BK = 16;
+constexpr int EX_THREADS = 256;
+
+template <typename T>
+struct ExactOps;
+template <>
+struct ExactOps<float> {
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+};
+template <>
+struct ExactOps<double> {
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+};
+
+struct ExactGroup {
+  bd_kv_problem p[BD_MAX_GROUP];
+  int tiles_n[BD_MAX_GROUP];
+  int tile_start[BD_MAX_GROUP + 1];
+  int count;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(EX_THREADS)
+    kv_proj_exact_kernel(const __grid_constant__ ExactGroup g, int* flag) {
+  // Locate the problem and the 64x64 tile this CTA owns.
+  int t = blockIdx.x;
+  int pi = 0;
+  while (pi + 1 < g.count && t >= g.tile_start[pi + 1]) ++pi;
+  const bd_kv_problem& P = g.p[pi];
+  const int local = t - g.tile_start[pi];
+  const int tn = local % g.tiles_n[pi];
+  const int tm = local / g.tiles_n[pi];
+  const int64_t m0 = static_cast<int64_t>(tm) * EX_BM;
+  const int64_t n0 = static_cast<int64_t>(tn) * EX_BN;
+
+  const T* __restrict__ x = static_cast<const T*>(P.x);
+  const T* __restrict__ c = static_cast<const T*>(P.c);
+  T* __restrict__ out = static_cast<T*>(P.out);
+  const int64_t K = P.d - P.d_h;
+  const int64_t N = P.n_heads * P.d_h;
+
+  __shared__ T xs[EX_BK][EX_BM];  // x slab, k-major so a thread's 4 rows are contiguous
+  __shared__ T cs[EX_BK][EX_BN];
+
+  const int tx = threadIdx.x % 16;  // column group
+  const int ty = threadIdx.x / 16;  // row group
+  T acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+
+  for (int64_t k0 = 0; k0 < K; k0 += EX_BK) {
+    // Stage x[m0:m0+64, mul_base+k0 : +16] and c[k0:k0+16, n0:n0+64] (zero-filled
+    // outside the problem; padded entries are never folded into acc, see kmax).
+    for (int e = threadIdx.x; e < EX_BM * EX_BK; e += EX_THREADS) {
+      const int r = e / EX_BK, kk = e % EX_BK;
+      const int64_t row = m0 + r, col = k0 + kk;
+      xs[kk][r] = (row < P.L && col < K) ? x[row * P.ldx + P.mul_base + col] : T(0);
+    }
+    for (int e = threadIdx.x; e < EX_BN * EX_BK; e += EX_THREADS) {
+      const int kk = e / EX_BN, cc = e % EX_BN;
+      const int64_t krow = k0 + kk, col = n0 + cc;
+      cs[kk][cc] = (krow < K && col < N) ? c[krow * P.ldc + col] : T(0);
+    }
+    __syncthreads();
+    const int kmax = static_cast<int>((K - k0) < EX_BK ? (K - k0) : EX_BK);
+    for (int kk = 0; kk < kmax; ++kk) {  // k ascending: the reference's order
+      T a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = xs[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = cs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          acc[i][j] = ExactOps<T>::add(acc[i][j], ExactOps<T>::mul(a[i], b[j]));
+    }
+    __syncthreads();
+  }
+
+  // Epilogue: + the repeated basis slice, after the full sum (attention.py:266-270).
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = m0 + ty * 4 + i;
+    if (row >= P.L) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t col = n0 + tx * 4 + j;
+      if (col >= N) continue;
+      const T rep = x[row * P.ldx + P.rep_base + (col % P.d_h)];
+      const T v = ExactOps<T>::add(acc[i][j], rep);
+      out[row * P.ldo + col] = v;
+      bad |= !isfinite(v);
+    }
+  }
+  if (flag != nullptr && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) {
+    atomicExch(flag, 1);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_exact(const bd_kv_problem* probs, int count, int dtype, int* flag,
+                         cudaStream_t stream) {
+  ExactGroup g{};
+  g.count = count;
+  int total = 0;
+  for (int i = 0; i < count; ++i) {
+    g.p[i] = probs[i];
+    const int64_t N = probs[i].n_heads * probs[i].d_h;
+    const int64_t tn = (N + EX_BN - 1) / EX_BN;
+    const int64_t tm = (probs[i].L + EX_BM - 1) / EX_BM;
+    g.tiles_n[i] = static_cast<int>(tn);
+    g.tile_start[i] = total;
+    total += static_cast<int>(tn * tm);
+  }
+  g.tile_start[count] = total;
+  if (total == 0) return cudaSuccess;
+  if (dtype == BD_F32) {
+    kv_proj_exact_kernel<float><<<total, EX_THREADS, 0, stream>>>(g, flag);
+  } else {
+    kv_proj_exact_kernel<double><<<total, EX_THREADS, 0, stream>>>(g, flag);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace bdk

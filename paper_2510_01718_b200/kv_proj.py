@@ -1,0 +1,241 @@
+"""The BD K/V projection operator — the drop-in for ``bdattn.fused_kv_proj``.
+
+    K'_h = X[:, S] + X[:, ~S] @ C_h          (ref: pkg/src/bdattn/attention.py:273-295)
+
+``fused_kv_proj`` keeps the reference's name, argument meaning, tag semantics and
+check order (PrecisionError, then ShapeError for c's rows, then for c's cols;
+attention.py:283-288) and raises ``ValueError`` on a non-finite result like the
+reference's ``Tensor2D._wrap`` (tensor.py:112-113).  Tensors are torch CUDA tensors;
+the arithmetic runs in the C-ABI library (libbd_kvproj.so):
+
+* float32 / float64 -> the exact SIMT kernel, bit-identical to the reference;
+* float16 / bfloat16 -> the sm_100a tcgen05 kernel (FP32 accumulate, fused
+  gather-add, one output rounding).
+
+There is no CPU fallback: CPU tensors raise.  ``fused_kv_proj_host`` is the
+synchronous host-buffer entry (numpy in, numpy out) that mirrors the reference's
+numba call boundary exactly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from enum import Enum
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import NativeLibraryError, PrecisionError, ShapeError
+
+
+class Tag(Enum):
+    """Which contiguous block serves as the basis (ref: decompose.py:27-31)."""
+
+    FIRST = "first"
+    LAST = "last"
+
+
+_DTYPES = {
+    torch.float32: N.BD_F32,
+    torch.float64: N.BD_F64,
+    torch.float16: N.BD_F16,
+    torch.bfloat16: N.BD_BF16,
+}
+_NP_DTYPES = {np.dtype(np.float32): N.BD_F32, np.dtype(np.float64): N.BD_F64,
+              np.dtype(np.float16): N.BD_F16}
+_MODES = {"auto": N.BD_MODE_AUTO, "exact": N.BD_MODE_EXACT, "tc": N.BD_MODE_TC}
+
+
+def tag_offsets(d: int, d_h: int, tag: Tag) -> tuple[int, int]:
+    """(mul_base, rep_base) for a tag (ref: attention.py:289-292)."""
+    if tag is Tag.FIRST:
+        return d_h, 0
+    if tag is Tag.LAST:
+        return 0, d - d_h
+    raise ValueError(f"unknown tag {tag!r}")
+
+
+def _rows_cols(t) -> tuple[int, int]:
+    if t.dim() != 2:
+        raise ShapeError(f"expected a 2-D tensor, got {t.dim()}-D")
+    return int(t.shape[0]), int(t.shape[1])
+
+
+def _check(x: torch.Tensor, c: torch.Tensor, d_h: int, n_heads: int) -> None:
+    # Same order as the reference (attention.py:283-288).
+    if x.dtype != c.dtype:
+        raise PrecisionError("x and c must share precision")
+    _, xcols = _rows_cols(x)
+    crows, ccols = _rows_cols(c)
+    if crows != xcols - d_h:
+        raise ShapeError(f"c has {crows} rows, expected d - d_h = {xcols - d_h}")
+    if ccols != n_heads * d_h:
+        raise ShapeError(f"c has {ccols} cols, expected n_heads * d_h = {n_heads * d_h}")
+    if x.dtype not in _DTYPES:
+        raise PrecisionError(f"unsupported dtype {x.dtype}; expected float32/64, float16, bfloat16")
+    if not (x.is_cuda and c.is_cuda):
+        raise NativeLibraryError(
+            "fused_kv_proj needs CUDA tensors (no CPU fallback); "
+            "use fused_kv_proj_host for host buffers")
+    if x.device != c.device:
+        raise ValueError(f"x on {x.device} but c on {c.device}")
+
+
+def _rowmajor(t: torch.Tensor) -> torch.Tensor:
+    return t if (t.stride(1) == 1 and t.stride(0) >= t.shape[1]) else t.contiguous()
+
+
+def _problem(x, c, out, d_h, n_heads, tag) -> N.KvProblem:
+    L, d = int(x.shape[0]), int(x.shape[1])
+    mul_base, rep_base = tag_offsets(d, d_h, tag)
+    return N.KvProblem(x.data_ptr(), c.data_ptr(), out.data_ptr(), x.stride(0), c.stride(0),
+                       out.stride(0), L, d, d_h, n_heads, mul_base, rep_base)
+
+
+def _finish(flag: torch.Tensor | None) -> None:
+    if flag is not None and int(flag.item()) != 0:
+        raise ValueError("operation produced non-finite values")
+
+
+def fused_kv_proj(x: torch.Tensor, c: torch.Tensor, d_h: int, n_heads: int,
+                  tag: Tag = Tag.FIRST, *, out: torch.Tensor | None = None,
+                  check_finite: bool = True, mode: str = "auto") -> torch.Tensor:
+    """Merged key/value projection in one pass over the output.
+
+    Equivalent to tiling one d_h-wide slice of x n_heads times and adding the
+    product of the complementary slice with c (FIRST repeats the leading slice,
+    LAST the trailing one), without materialising the repeat or the slice.
+    Enqueued on the current CUDA stream; ``check_finite`` synchronises once to
+    read the kernel's non-finite flag (pass False on latency-critical paths).
+    """
+    _check(x, c, d_h, n_heads)
+    x = _rowmajor(x)
+    c = _rowmajor(c)
+    L = int(x.shape[0])
+    if out is None:
+        out = torch.empty((L, n_heads * d_h), dtype=x.dtype, device=x.device)
+    elif out.shape != (L, n_heads * d_h) or out.dtype != x.dtype or out.stride(1) != 1:
+        raise ShapeError("out must be a row-major (L, n_heads*d_h) tensor of x's dtype")
+    flag = torch.zeros(1, dtype=torch.int32, device=x.device) if check_finite else None
+    prob = _problem(x, c, out, d_h, n_heads, tag)
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    with torch.cuda.device(x.device):
+        st = N.load().bd_kv_proj_grouped(ctypes.byref(prob), 1, _DTYPES[x.dtype], _MODES[mode],
+                                         flag.data_ptr() if flag is not None else None, stream)
+    N.check(st, "bd_kv_proj")
+    _finish(flag)
+    return out
+
+
+def fused_kv_proj_grouped(x: torch.Tensor,
+                          specs: Sequence[tuple[torch.Tensor, int, int, Tag]],
+                          *, outs: Sequence[torch.Tensor] | None = None,
+                          check_finite: bool = False, mode: str = "auto",
+                          flag: torch.Tensor | None = None) -> list[torch.Tensor]:
+    """Several projections of the same x in ONE kernel launch.
+
+    ``specs`` is a list of (c, d_h, n_heads, tag) — e.g. K' and V' of
+    ``bda_forward`` (ref attention.py:305-306), whose tags may differ.
+    """
+    if not 1 <= len(specs) <= N.BD_MAX_GROUP:
+        raise ValueError(f"between 1 and {N.BD_MAX_GROUP} projections per launch")
+    x = _rowmajor(x)
+    probs = (N.KvProblem * len(specs))()
+    results = []
+    for i, (c, d_h, n_heads, tag) in enumerate(specs):
+        _check(x, c, d_h, n_heads)
+        c = _rowmajor(c)
+        if outs is not None:
+            o = outs[i]
+        else:
+            o = torch.empty((x.shape[0], n_heads * d_h), dtype=x.dtype, device=x.device)
+        probs[i] = _problem(x, c, o, d_h, n_heads, tag)
+        results.append(o)
+    own_flag = flag is None and check_finite
+    if own_flag:
+        flag = torch.zeros(1, dtype=torch.int32, device=x.device)
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    with torch.cuda.device(x.device):
+        st = N.load().bd_kv_proj_grouped(probs, len(specs), _DTYPES[x.dtype], _MODES[mode],
+                                         flag.data_ptr() if flag is not None else None, stream)
+    N.check(st, "bd_kv_proj_grouped")
+    if own_flag:
+        _finish(flag)
+    return results
+
+
+_staging: dict = {}
+
+
+def fused_kv_proj_grouped_host(x_host: torch.Tensor,
+                               specs: Sequence[tuple[torch.Tensor, int, int, Tag]],
+                               *, outs: Sequence[torch.Tensor] | None = None,
+                               mode: str = "auto") -> list[torch.Tensor]:
+    """Grouped projection of a HOST activation tensor against device-resident C's.
+
+    Copies x in (H2D, asynchronous when x is pinned), runs the grouped kernel, copies
+    every projection out (D2H into ``outs``, pinned host tensors, or new ones) and
+    synchronises, so the returned host tensors are ready — the end-to-end path of a
+    caller whose activations live on the host.
+    """
+    if x_host.is_cuda:
+        raise ValueError("x_host must be a host tensor; use fused_kv_proj_grouped")
+    dev = specs[0][0].device
+    key = (dev, tuple(x_host.shape), x_host.dtype)
+    xd = _staging.get(key)
+    if xd is None:
+        xd = _staging[key] = torch.empty(x_host.shape, dtype=x_host.dtype, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    xd.copy_(x_host, non_blocking=True)
+    res = fused_kv_proj_grouped(xd, specs, mode=mode)
+    if outs is None:
+        outs = [torch.empty(r.shape, dtype=r.dtype, pin_memory=True) for r in res]
+    for o, r in zip(outs, res):
+        o.copy_(r, non_blocking=True)
+    stream.synchronize()
+    return list(outs)
+
+
+def fused_kv_proj_host(x: np.ndarray, c: np.ndarray, d_h: int, n_heads: int,
+                       tag: Tag = Tag.FIRST, *, mode: str = "auto") -> np.ndarray:
+    """Synchronous host-buffer projection through ``bd_kv_proj_host``.
+
+    Takes and returns C-contiguous numpy arrays (float32/float64/float16), exactly
+    the boundary of the reference's numba kernel call (attention.py:293-295):
+    copies in, runs on the GPU, copies out.
+    """
+    if x.dtype != c.dtype:
+        raise PrecisionError("x and c must share precision")
+    if x.ndim != 2 or c.ndim != 2:
+        raise ShapeError("expected 2-D arrays")
+    if c.shape[0] != x.shape[1] - d_h:
+        raise ShapeError(f"c has {c.shape[0]} rows, expected d - d_h = {x.shape[1] - d_h}")
+    if c.shape[1] != n_heads * d_h:
+        raise ShapeError(f"c has {c.shape[1]} cols, expected n_heads * d_h = {n_heads * d_h}")
+    if x.dtype not in _NP_DTYPES:
+        raise PrecisionError(f"unsupported dtype {x.dtype}")
+    x = np.ascontiguousarray(x)
+    c = np.ascontiguousarray(c)
+    L, d = x.shape
+    mul_base, rep_base = tag_offsets(d, d_h, tag)
+    out = np.empty((L, n_heads * d_h), dtype=x.dtype)
+    bad = ctypes.c_int(0)
+    st = N.load().bd_kv_proj_host(x.ctypes.data, c.ctypes.data, out.ctypes.data, L, d, d_h,
+                                  n_heads, mul_base, rep_base, _NP_DTYPES[x.dtype], _MODES[mode],
+                                  ctypes.byref(bad))
+    N.check(st, "bd_kv_proj_host")
+    if bad.value:
+        raise ValueError("operation produced non-finite values")
+    return out
+
+
+def kv_flops(L: int, d: int, d_h: int, n_heads: int) -> int:
+    """Multiply-FLOPs of one BD projection: 2 L (d - d_h) N (ref bench.py:158 ratio)."""
+    return 2 * L * (d - d_h) * n_heads * d_h
+
+
+def flop_ratio(d: int, d_h: int) -> float:
+    """Dense / BD FLOP ratio d / (d - d_h) (ref: bench.py:266)."""
+    return d / (d - d_h)

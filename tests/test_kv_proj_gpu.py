@@ -1,0 +1,242 @@
+"""GPU parity of the BD K/V projection against the reference (golden vectors) and the
+CPU oracle.  All calls go through the C-ABI library (libbd_kvproj.so).
+
+Tolerances:
+  * float32 / float64 (exact kernel): bit-identical to the reference.
+  * float16 (tensor cores): max_relative_error <= 1e-3 against the FP64 oracle on the
+    same rounded inputs, plus the elementwise bound
+    |out - ref| <= 2 u16 |ref| + 2 K u32 sum_k |x||c| + u16 * |x_rep|.
+  * bfloat16: max_relative_error <= 8e-3 and the same elementwise bound with u_bf16.
+"""
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+import paper_2510_01718_b200 as bd
+from paper_2510_01718_b200 import _native as N
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+U16 = {torch.float16: 2.0 ** -11, torch.bfloat16: 2.0 ** -8}
+MAXREL = {torch.float16: 1e-3, torch.bfloat16: 8e-3}
+U32 = 2.0 ** -24
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def to_np64(t: torch.Tensor) -> np.ndarray:
+    return t.detach().to("cpu", torch.float64).numpy()
+
+
+def assert_tc_close(got: torch.Tensor, x: torch.Tensor, c: torch.Tensor, d_h, n, tag, rows=None):
+    """Compare a 16-bit kernel output with the FP64 oracle on identical rounded inputs."""
+    xs = x if rows is None else x[rows]
+    g = got if rows is None else got[rows]
+    x64, c64 = to_np64(xs), to_np64(c)
+    ref = O.fused_kv_proj_ref(x64, c64, d_h, n, tag.value, threads=O.default_threads())
+    mul_base, rep_base = bd.tag_offsets(x64.shape[1], d_h, tag)
+    K = x64.shape[1] - d_h
+    absprod = O.fused_kv_proj_ref(np.abs(x64), np.abs(c64), d_h, n, tag.value,
+                                  threads=O.default_threads())  # sum|x||c| + |x_rep|
+    g64 = to_np64(g)
+    u = U16[got.dtype]
+    bound = 2 * u * np.abs(ref) + 2 * K * U32 * absprod + 1e-30
+    err = np.abs(g64 - ref)
+    worst = float((err / bound).max())
+    assert worst <= 1.0, f"elementwise bound exceeded by {worst:.3g}x"
+    assert O.max_relative_error(g64, ref) <= MAXREL[got.dtype]
+
+
+# ------------------------------------------------------------------ exact path
+@pytest.fixture(scope="module")
+def small():
+    meta = json.loads((GOLDEN / "fused_small.json").read_text())
+    return meta, np.load(GOLDEN / "fused_small.npz")
+
+
+def test_exact_kernel_bit_identical_on_every_reference_case(small, cuda):
+    meta, arrs = small
+    for i, m in enumerate(meta):
+        x = torch.from_numpy(arrs[f"x{i}"]).to(cuda)
+        c = torch.from_numpy(arrs[f"c{i}"]).to(cuda)
+        out = bd.fused_kv_proj(x, c, m["d_h"], m["n_heads"], bd.Tag(m["tag"]))
+        np.testing.assert_array_equal(out.cpu().numpy(), arrs[f"out{i}"], err_msg=m["source"])
+
+
+def test_exact_cfg1_k_and_v_match_reference_hashes(cuda):
+    meta = json.loads((GOLDEN / "cfg1.json").read_text())
+    g = np.load(GOLDEN / "cfg1.npz")
+    x = torch.from_numpy(O.rand_gaussian(O.Rng(8), 256, 512, np.float32)).to(cuda)
+    k = bd.fused_kv_proj(x, torch.from_numpy(g["c_qk"]).to(cuda), 64, 8, bd.Tag(meta["qk_tag"]))
+    v = bd.fused_kv_proj(x, torch.from_numpy(g["c_vo"]).to(cuda), 64, 8, bd.Tag(meta["vo_tag"]))
+    assert sha(k.cpu().numpy()) == meta["k_out_sha256"]
+    assert sha(v.cpu().numpy()) == meta["v_out_sha256"]
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("shape", [(1, 9, 3, 2), (300, 200, 40, 3), (129, 77, 13, 5),
+                                   (1000, 520, 136, 4)])
+def test_exact_kernel_matches_oracle_random_shapes(dtype, shape, cuda):
+    L, d, d_h, n = shape
+    rng = O.Rng(sum(shape))
+    x = O.rand_gaussian(rng, L, d, dtype)
+    c = O.rand_gaussian(rng, d - d_h, n * d_h, dtype)
+    for tag in bd.Tag:
+        out = bd.fused_kv_proj(torch.from_numpy(x).to(cuda), torch.from_numpy(c).to(cuda), d_h, n,
+                               tag)
+        np.testing.assert_array_equal(out.cpu().numpy(),
+                                      O.fused_kv_proj_ref(x, c, d_h, n, tag.value, threads=8))
+
+
+def test_exact_grouped_launch_equals_separate(cuda):
+    rng = O.Rng(11)
+    x = torch.from_numpy(O.rand_gaussian(rng, 70, 48, np.float32)).to(cuda)
+    ck = torch.from_numpy(O.rand_gaussian(rng, 40, 24, np.float32)).to(cuda)
+    cv = torch.from_numpy(O.rand_gaussian(rng, 40, 24, np.float32)).to(cuda)
+    k, v = bd.fused_kv_proj_grouped(x, [(ck, 8, 3, bd.Tag.FIRST), (cv, 8, 3, bd.Tag.LAST)])
+    torch.testing.assert_close(k, bd.fused_kv_proj(x, ck, 8, 3, bd.Tag.FIRST), rtol=0, atol=0)
+    torch.testing.assert_close(v, bd.fused_kv_proj(x, cv, 8, 3, bd.Tag.LAST), rtol=0, atol=0)
+
+
+def test_non_finite_result_raises(cuda):
+    x = torch.ones(4, 10, device=cuda)
+    x[1, 5] = float("inf")
+    c = torch.ones(7, 9, device=cuda)
+    with pytest.raises(ValueError, match="non-finite"):
+        bd.fused_kv_proj(x, c, 3, 3)
+    xh = x.half()
+    with pytest.raises(ValueError, match="non-finite"):
+        bd.fused_kv_proj(torch.nn.functional.pad(xh, (0, 6)), torch.ones(8, 16, device=cuda).half(),
+                         8, 2)
+
+
+def test_host_entry_point_bit_exact(cuda):
+    rng = O.Rng(21)
+    x = O.rand_gaussian(rng, 33, 50, np.float32)
+    c = O.rand_gaussian(rng, 40, 30, np.float32)
+    np.testing.assert_array_equal(bd.fused_kv_proj_host(x, c, 10, 3, bd.Tag.LAST),
+                                  O.fused_kv_proj_ref(x, c, 10, 3, "last"))
+
+
+# ------------------------------------------------------------------ tensor-core path
+TC_SHAPES = [
+    # L, d, d_h, n_heads
+    (256, 512, 64, 8),      # cfg1 geometry
+    (1000, 512, 128, 16),   # DSV2-Lite kv_b_proj half, ragged L
+    (128, 328, 64, 3),      # K=264 (not a multiple of 64), N=192 (< one 256 tile)
+    (77, 136, 8, 5),        # tiny d_h, N=40
+    (300, 1024, 128, 7),    # N = 896: last tile partial
+]
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("shape", TC_SHAPES)
+def test_tc_kernel_matches_fp64_oracle(dtype, shape, cuda):
+    L, d, d_h, n = shape
+    g = torch.Generator().manual_seed(L * 7 + d)
+    x = torch.randn(L, d, generator=g).to(dtype).to(cuda)
+    c = (torch.randn(d - d_h, n * d_h, generator=g) / 4).to(dtype).to(cuda)
+    for tag in bd.Tag:
+        out = bd.fused_kv_proj(x, c, d_h, n, tag)
+        assert out.dtype == dtype
+        assert_tc_close(out, x, c, d_h, n, tag)
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_tc_cfg2_full_size_sampled_rows(dtype, cuda):
+    """DSV2-Lite kv_b_proj, 8192 tokens, K and V in one launch (BASELINE config 2)."""
+    L, d, d_h, n = 8192, 512, 128, 16
+    g = torch.Generator().manual_seed(2)
+    x = torch.randn(L, d, generator=g).to(dtype).to(cuda)
+    ck = (torch.randn(d - d_h, n * d_h, generator=g) / 8).to(dtype).to(cuda)
+    cv = (torch.randn(d - d_h, n * d_h, generator=g) / 8).to(dtype).to(cuda)
+    k, v = bd.fused_kv_proj_grouped(x, [(ck, d_h, n, bd.Tag.FIRST), (cv, d_h, n, bd.Tag.LAST)],
+                                    check_finite=True)
+    rows = torch.randperm(L, generator=g)[:96].sort().values
+    rows = torch.cat([rows, torch.tensor([0, 127, 128, L - 1])])
+    assert_tc_close(k, x, ck, d_h, n, bd.Tag.FIRST, rows=rows.to(cuda))
+    assert_tc_close(v, x, cv, d_h, n, bd.Tag.LAST, rows=rows.to(cuda))
+    # size-independent properties over the FULL output:
+    # (1) zero coefficients -> exact repeat of the basis slice
+    z = bd.fused_kv_proj(x, torch.zeros_like(ck), d_h, n, bd.Tag.FIRST)
+    torch.testing.assert_close(z, x[:, :d_h].repeat(1, n), rtol=0, atol=0)
+    # (2) scaling x by 2 is exact in binary floating point -> output doubles exactly
+    #     (wherever the result is a normal number: subnormal outputs round on an absolute
+    #     grid, so round(2v) and 2 round(v) may differ there)
+    k2 = bd.fused_kv_proj(x * 2, ck, d_h, n, bd.Tag.FIRST)
+    normal = k.float().abs() >= torch.finfo(dtype).tiny * 2
+    assert int(normal.sum()) > 0.99 * k.numel()
+    torch.testing.assert_close(k2[normal], (k * 2)[normal], rtol=0, atol=0)
+    # (3) grouped launch == separate launches, bit for bit
+    torch.testing.assert_close(bd.fused_kv_proj(x, cv, d_h, n, bd.Tag.LAST), v, rtol=0, atol=0)
+
+
+def test_tc_matches_cublas_dense_with_rewritten_weight(cuda):
+    """Kernel vs cuBLAS X @ W' where W' = [I; C] per head (the BD-rewritten dense weight):
+    same math, different summation -> within FP16 rounding."""
+    L, d, d_h, n = 2048, 512, 128, 16
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(L, d, generator=g).half().to(cuda)
+    c = (torch.randn(d - d_h, n * d_h, generator=g) / 8).half().to(cuda)
+    eye = torch.eye(d_h, dtype=torch.float16, device=cuda).repeat(1, n)
+    w_dense = torch.cat([eye, c], dim=0)  # FIRST tag: identity rows at S = [0, d_h)
+    dense = x @ w_dense
+    ours = bd.fused_kv_proj(x, c, d_h, n, bd.Tag.FIRST)
+    rel = (ours.float() - dense.float()).abs().max() / dense.float().abs().max()
+    assert float(rel) < 2e-3
+
+
+def test_tc_head_shards_are_bit_identical(cuda):
+    """Column (head) shards of c give bit-identical columns: the multi-GPU invariant."""
+    L, d, d_h, n = 512, 512, 128, 16
+    g = torch.Generator().manual_seed(9)
+    x = torch.randn(L, d, generator=g).half().to(cuda)
+    c = (torch.randn(d - d_h, n * d_h, generator=g) / 8).half().to(cuda)
+    full = bd.fused_kv_proj(x, c, d_h, n, bd.Tag.LAST)
+    for world in (2, 4, 8):
+        per = n // world
+        for r in range(world):
+            cs = c[:, r * per * d_h:(r + 1) * per * d_h].contiguous()
+            part = bd.fused_kv_proj(x, cs, d_h, per, bd.Tag.LAST)
+            torch.testing.assert_close(part, full[:, r * per * d_h:(r + 1) * per * d_h],
+                                       rtol=0, atol=0)
+
+
+def test_tc_strided_views(cuda):
+    """Row-strided x/out views (e.g. a slice of a larger activation buffer) are honoured."""
+    L, d, d_h, n = 200, 256, 64, 4
+    g = torch.Generator().manual_seed(3)
+    big = torch.randn(L, d + 64, generator=g).half().to(cuda)
+    x = big[:, 32:32 + d]
+    c = (torch.randn(d - d_h, n * d_h, generator=g) / 4).half().to(cuda)
+    obuf = torch.full((L, n * d_h + 16), 7.0, dtype=torch.float16, device=cuda)
+    out = obuf[:, 8:8 + n * d_h]
+    bd.fused_kv_proj(x, c, d_h, n, bd.Tag.FIRST, out=out)
+    assert_tc_close(out, x, c, d_h, n, bd.Tag.FIRST)
+    assert bool((obuf[:, :8] == 7).all()) and bool((obuf[:, 8 + n * d_h:] == 7).all())
+
+
+def test_tc_host_entry_point(cuda):
+    rng = O.Rng(4)
+    x = O.rand_gaussian(rng, 300, 256, np.float16)
+    c = (O.rand_gaussian(rng, 192, 256, np.float32) / 4).astype(np.float16)
+    out = bd.fused_kv_proj_host(x, c, 64, 4, bd.Tag.FIRST)
+    assert_tc_close(torch.from_numpy(out), torch.from_numpy(x), torch.from_numpy(c), 64, 4,
+                    bd.Tag.FIRST)
+
+
+def test_launch_counter_counts_our_kernels(cuda):
+    x = torch.randn(64, 64, device=cuda).half()
+    c = torch.randn(32, 64, device=cuda).half()
+    before = N.launch_count()
+    bd.fused_kv_proj(x, c, 32, 2, check_finite=False)
+    torch.cuda.synchronize()
+    assert N.launch_count() == before + 1
