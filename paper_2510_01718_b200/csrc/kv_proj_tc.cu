@@ -27,6 +27,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -40,24 +41,31 @@ constexpr int BM = 128;                       // UMMA M (rows of x per tile)
 constexpr int BN = 256;                       // UMMA N (output columns per tile)
 constexpr int BK = 64;                        // k-block: one 128-byte swizzle row of A
 constexpr int UK = 16;                        // UMMA K for kind::f16
-constexpr int STAGES = 4;                     // smem ring depth
-constexpr int EPI_WARPS = 4;                  // 128 epilogue threads = 128 TMEM lanes
+constexpr int STAGES = 3;                     // smem ring depth (A+B)
+constexpr int EPI_WARPS = 8;                  // 2 per SMSP; warps w, w+4 share a TMEM lane quadrant
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr uint32_t A_BYTES = BM * BK * 2;     // 16 KiB
 constexpr uint32_t B_CHUNK = 64 * BK * 2;     // one 64-column MN-major swizzle panel, 8 KiB
 constexpr uint32_t B_BYTES = BN * BK * 2;     // 32 KiB
 constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr uint32_t REP_BOX = 64 * BM * 2;     // one 64-column x 128-row rep box, 16 KiB
+constexpr uint32_t REP_BYTES = 2 * REP_BOX;   // d_h <= 128 -> at most two boxes
+constexpr uint32_t STG_BYTES = 32 * 32 * 2;   // per-warp output staging: 32 rows x 32 cols (SW64)
 constexpr uint32_t TMEM_COLS = 2 * BN;        // double-buffered accumulator
-constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+constexpr size_t SMEM_BYTES =
+    1024 + STAGES * STAGE_BYTES + 2 * REP_BYTES + EPI_WARPS * STG_BYTES + 256;
+static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
 struct TcProblem {
-  CUtensorMap map_a;  // x + mul_base, dims {K, L}, box {64, 128}
-  CUtensorMap map_b;  // c,            dims {N, K}, box {64, 64}
+  CUtensorMap map_a;    // x + mul_base, dims {K, L},   box {64, 128}
+  CUtensorMap map_b;    // c,            dims {N, K},   box {64, 64}
+  CUtensorMap map_rep;  // x + rep_base, dims {d_h, L}, box {64, 128}   (rep_fast only)
+  CUtensorMap map_out;  // out,          dims {N, L},   box {32, 32}, SW64
   const void* x;
-  void* out;
-  int64_t ldx, ldo;
+  int64_t ldx;
   int32_t L, N, K, d_h, rep_base;
   int32_t tiles_n, num_kb, tile_start;
+  int32_t rep_fast;     // d_h in {64, 128}: rep tile staged in smem by TMA
 };
 
 struct TcParams {
@@ -65,6 +73,7 @@ struct TcParams {
   int32_t count;
   int32_t total_tiles;
   int* flag;
+  int32_t debug;  // profiling knob (env BD_TC_DEBUG): 1 no stores, 2 no epilogue math, 4 no LDTM
 };
 
 __device__ __forceinline__ void decode_tile(const TcParams& prm, int t, int& pi, int& m0,
@@ -75,6 +84,9 @@ __device__ __forceinline__ void decode_tile(const TcParams& prm, int t, int& pi,
   n0 = (local % prm.p[pi].tiles_n) * BN;
   m0 = (local / prm.p[pi].tiles_n) * BM;
 }
+
+// Tiles sharing (problem, m-block) share the rep tile x[m0:m0+128, rep_base:+d_h].
+__device__ __forceinline__ int rep_key(int pi, int m0) { return (pi << 24) | (m0 / BM); }
 
 template <bool kBF16>
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -98,11 +110,11 @@ __device__ __forceinline__ float2 unpack2(uint32_t w) {
   }
 }
 
-// True if either 16-bit half of w is Inf/NaN (exponent all ones).
-template <bool kBF16>
-__device__ __forceinline__ bool nonfinite2(uint32_t w) {
-  constexpr uint32_t E = kBF16 ? 0x7F80u : 0x7C00u;
-  return ((w & E) == E) || (((w >> 16) & E) == E);
+// max that propagates NaN (PTX max.NaN), so one running value flags NaN and overflow.
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
 }
 
 template <bool kBF16>
@@ -112,20 +124,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint8_t* sB = sA + STAGES * A_BYTES;
+  uint8_t* sRep = sB + STAGES * B_BYTES;            // 2 slots x REP_BYTES
+  uint8_t* sStg = sRep + 2 * REP_BYTES;             // EPI_WARPS x STG_BYTES
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + EPI_WARPS * STG_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rfull = tempty + 2;
+  uint64_t* rempty = rfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + 2);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  // Contiguous tile range per CTA: consecutive tiles share the x row-block (A and the
+  // rep slice stay L2/smem-hot); the split is balanced to within one tile.
+  const int t_begin = static_cast<int>(static_cast<int64_t>(blockIdx.x) * prm.total_tiles / gridDim.x);
+  const int t_end = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * prm.total_tiles / gridDim.x);
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < prm.count; ++i) {
       tma_prefetch_desc(&prm.p[i].map_a);
       tma_prefetch_desc(&prm.p[i].map_b);
+      tma_prefetch_desc(&prm.p[i].map_out);
+      if (prm.p[i].rep_fast) tma_prefetch_desc(&prm.p[i].map_rep);
     }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -133,7 +155,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EPI_WARPS);
+      mbar_init(&tempty[a], 1);
+      mbar_init(&rfull[a], 1);
+      mbar_init(&rempty[a], 1);
     }
     fence_mbar_init();
   }
@@ -152,10 +176,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pol = policy_evict_last();  // x and c are re-read; out streams past
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < prm.total_tiles; t += gridDim.x) {
+      int rslot = 1;
+      uint32_t rphase = 0;  // bit s = parity of rep slot s
+      int prev_key = -1;
+      for (int t = t_begin; t < t_end; ++t) {
         int pi, m0, n0;
         decode_tile(prm, t, pi, m0, n0);
         const TcProblem& P = prm.p[pi];
+        const int key = rep_key(pi, m0);
+        if (P.rep_fast && key != prev_key) {
+          // New (problem, m-block): stage its rep tile in the other slot.
+          rslot ^= 1;
+          mbar_wait(&rempty[rslot], ((rphase >> rslot) & 1u) ^ 1u);
+          rphase ^= 1u << rslot;
+          const int nbox = P.d_h / 64;
+          mbar_arrive_expect_tx(&rfull[rslot], nbox * REP_BOX);
+          for (int b = 0; b < nbox; ++b)
+            tma_load_2d(sRep + rslot * REP_BYTES + b * REP_BOX, &P.map_rep, 64 * b, m0,
+                        &rfull[rslot], pol);
+        }
+        prev_key = key;
         for (int kb = 0; kb < P.num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
@@ -179,7 +219,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < prm.total_tiles; t += gridDim.x, ++it) {
+      for (int t = t_begin; t < t_end; ++t, ++it) {
         int pi, m0, n0;
         decode_tile(prm, t, pi, m0, n0);
         const TcProblem& P = prm.p[pi];
@@ -214,55 +254,132 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
-    const int row_in_tile = static_cast<int>(quad * 32 + lane);
-    bool bad = false;
+    // 8 warps: warp w reads TMEM lanes 32*(w%4).. (its quadrant) and columns
+    // [128*h, 128*h+128) of the accumulator, h = (w-2)/4, in four 32-column sub-chunks;
+    // the TMEM load of sub-chunk i+1 is in flight while sub-chunk i is processed.
+    const uint32_t ew = warp - 2;
+    const uint32_t quad = warp & 3;
+    const uint32_t half = ew >> 2;
+    const int row_w = static_cast<int>(lane);
+    const int row_t = static_cast<int>(quad * 32) + row_w;
+    const bool leader = (ew == 0 && lane == 0);
+    uint8_t* stg = sStg + ew * STG_BYTES;
+    const uint32_t stg_u32 = smem_u32(stg);
+    const uint32_t stg_row = stg_u32 + row_w * 64;
+    const uint32_t sw64 = static_cast<uint32_t>((row_w >> 1) & 3);
+    float amax = 0.f;  // NaN-propagating max |out| for the non-finite check
+    int rslot = 1;
+    uint32_t rphase = 0;  // bit s = parity of rep slot s
+    int prev_key = -1;
     int it = 0;
-    for (int t = blockIdx.x; t < prm.total_tiles; t += gridDim.x, ++it) {
+    for (int t = t_begin; t < t_end; ++t, ++it) {
       int pi, m0, n0;
       decode_tile(prm, t, pi, m0, n0);
       const TcProblem& P = prm.p[pi];
+      const int key = rep_key(pi, m0);
+      const bool fast = P.rep_fast != 0;
+      if (fast && key != prev_key) {
+        rslot ^= 1;
+        mbar_wait(&rfull[rslot], (rphase >> rslot) & 1u);
+        rphase ^= 1u << rslot;
+      }
+      prev_key = key;
+      const uint8_t* rep_row = sRep + rslot * REP_BYTES + row_t * 128;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t row = static_cast<int64_t>(m0) + row_in_tile;
-      const bool row_ok = row < P.L;
-      const uint16_t* xrow =
-          static_cast<const uint16_t*>(P.x) + (row_ok ? row : 0) * P.ldx + P.rep_base;
-      uint16_t* orow = static_cast<uint16_t*>(P.out) + (row_ok ? row : 0) * P.ldo;
-      const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * BN;
-#pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr + ch * 32, r);
-        tmem_ld_wait();
-        if (row_ok) {
+      const int64_t grow = static_cast<int64_t>(m0) + row_t;
+      const uint16_t* xrow = static_cast<const uint16_t*>(P.x) +
+                             (grow < P.L ? grow : 0) * P.ldx + P.rep_base;
+      const int cbase = n0 + static_cast<int>(half) * 128;
+      int nsub = (P.N - cbase + 31) / 32;
+      nsub = nsub < 0 ? 0 : (nsub > 4 ? 4 : nsub);
+      const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * BN + half * 128;
+      const int dmask = P.d_h - 1;
+
+      auto process = [&](const uint32_t (&r)[32], int sub) {
+        const int col0 = cbase + sub * 32;
+        uint4 xv[4];
+        if (fast) {
+          const int jj0 = col0 & dmask;  // d_h in {64,128}: 32 columns never wrap a head
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
-            const int col = n0 + ch * 32 + g * 8;
-            if (col < P.N) {
-              const int jj = col % P.d_h;  // 8 columns never straddle a head (d_h % 8 == 0)
-              const uint4 xv = __ldg(reinterpret_cast<const uint4*>(xrow + jj));
-              const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
-              uint32_t o[4];
+            const int jj = jj0 + 8 * g;
+            const uint32_t ch = static_cast<uint32_t>((jj & 63) >> 3);
+            xv[g] = *reinterpret_cast<const uint4*>(rep_row + (jj >> 6) * REP_BOX +
+                                                    ((ch ^ (row_t & 7)) << 4));
+          }
+        } else {
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 xr = unpack2<kBF16>(xw[e]);
-                const float v0 = __fadd_rn(__uint_as_float(r[g * 8 + 2 * e]), xr.x);
-                const float v1 = __fadd_rn(__uint_as_float(r[g * 8 + 2 * e + 1]), xr.y);
-                o[e] = pack2<kBF16>(v0, v1);
-                bad |= nonfinite2<kBF16>(o[e]);
-              }
-              *reinterpret_cast<uint4*>(orow + col) = make_uint4(o[0], o[1], o[2], o[3]);
-            }
+          for (int g = 0; g < 4; ++g) {
+            const int col = col0 + 8 * g;
+            xv[g] = (col < P.N && grow < P.L)
+                        ? __ldg(reinterpret_cast<const uint4*>(xrow + (col % P.d_h)))
+                        : make_uint4(0, 0, 0, 0);
           }
         }
+        if (lane == 0) tma_store_wait_read<0>();  // staging free again
+        __syncwarp();
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const uint32_t xw[4] = {xv[g].x, xv[g].y, xv[g].z, xv[g].w};
+          uint32_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 xr = unpack2<kBF16>(xw[e]);
+            const float v0 = __fadd_rn(__uint_as_float(r[8 * g + 2 * e]), xr.x);
+            const float v1 = __fadd_rn(__uint_as_float(r[8 * g + 2 * e + 1]), xr.y);
+            amax = fmax_nan(amax, fabsf(v0));
+            amax = fmax_nan(amax, fabsf(v1));
+            o[e] = pack2<kBF16>(v0, v1);
+          }
+          const uint32_t dst = stg_row + ((static_cast<uint32_t>(g) ^ sw64) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(o[0]),
+                       "r"(o[1]), "r"(o[2]), "r"(o[3])
+                       : "memory");
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && !(prm.debug & 1)) {
+          tma_store_2d(&P.map_out, stg, col0, m0 + static_cast<int>(quad) * 32);
+          tma_store_commit();
+        }
+      };
+
+      if (!(prm.debug & 4) && nsub > 0) {
+        uint32_t ra[32], rb[32];
+        tmem_ld_32x32b_x32(taddr, ra);
+#pragma unroll
+        for (int sub = 0; sub < 4; sub += 2) {
+          if (sub < nsub) {
+            tmem_ld_wait();
+            if (sub + 1 < nsub) tmem_ld_32x32b_x32(taddr + (sub + 1) * 32, rb);
+            if (!(prm.debug & 2)) process(ra, sub);
+          }
+          if (sub + 1 < nsub) {
+            tmem_ld_wait();
+            if (sub + 2 < nsub) tmem_ld_32x32b_x32(taddr + (sub + 2) * 32, ra);
+            if (!(prm.debug & 2)) process(rb, sub + 1);
+          }
+        }
+        if (prm.debug & 2) amax = fmax_nan(amax, __uint_as_float(ra[0] & 1u));
       }
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      named_bar_sync(1, 32 * EPI_WARPS);  // all epilogue threads finished with TMEM + rep
+      if (leader) {
+        mbar_arrive(&tempty[acc]);
+        if (fast) {
+          int npi = -1, nm0 = 0, nn0 = 0;
+          if (t + 1 < t_end) decode_tile(prm, t + 1, npi, nm0, nn0);
+          if (t + 1 >= t_end || rep_key(npi, nm0) != key) mbar_arrive(&rempty[rslot]);
+        }
+      }
     }
+    if (lane == 0) tma_store_wait_all<0>();
+    // values at or beyond the rounding threshold become Inf in the 16-bit output
+    const float limit = kBF16 ? __uint_as_float(0x7F7F8000u) : 65520.f;
+    const bool bad = !(amax < limit);
     if (prm.flag != nullptr && __any_sync(0xffffffffu, bad) && lane == 0) atomicExch(prm.flag, 1);
   }
 
@@ -291,7 +408,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // Row-major [rows x cols] 16-bit matrix, row stride ld elements, box {box_cols, box_rows}.
 bool encode_2d(CUtensorMap* map, const void* base, bool bf16, uint64_t cols, uint64_t rows,
-               uint64_t ld, uint32_t box_cols, uint32_t box_rows, std::string* err) {
+               uint64_t ld, uint32_t box_cols, uint32_t box_rows, std::string* err,
+               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (fn == nullptr) {
     *err = "cuTensorMapEncodeTiled unavailable from the driver";
@@ -303,7 +421,7 @@ bool encode_2d(CUtensorMap* map, const void* base, bool bf16, uint64_t cols, uin
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                   2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char buf[160];
@@ -330,15 +448,18 @@ int launch_tc(const bd_kv_problem* probs, int count, int dtype, int* flag, cudaS
     const int64_t N = q.n_heads * q.d_h;
     std::string err;
     const auto* xb = static_cast<const uint16_t*>(q.x) + q.mul_base;
+    const bool rep_fast = (q.d_h % 64 == 0) && q.d_h <= 128;
+    const auto* xr = static_cast<const uint16_t*>(q.x) + q.rep_base;
     if (!encode_2d(&P.map_a, xb, bf16, K, q.L, q.ldx, BK, BM, &err) ||
-        !encode_2d(&P.map_b, q.c, bf16, N, K, q.ldc, 64, BK, &err)) {
+        !encode_2d(&P.map_b, q.c, bf16, N, K, q.ldc, 64, BK, &err) ||
+        !encode_2d(&P.map_out, q.out, bf16, N, q.L, q.ldo, 32, 32, &err, CU_TENSOR_MAP_SWIZZLE_64B) ||
+        (rep_fast && !encode_2d(&P.map_rep, xr, bf16, q.d_h, q.L, q.ldx, 64, BM, &err))) {
       set_error(err);
       return BD_ERR_CUDA;
     }
+    P.rep_fast = rep_fast ? 1 : 0;
     P.x = q.x;
-    P.out = q.out;
     P.ldx = q.ldx;
-    P.ldo = q.ldo;
     P.L = static_cast<int32_t>(q.L);
     P.N = static_cast<int32_t>(N);
     P.K = static_cast<int32_t>(K);
@@ -351,6 +472,11 @@ int launch_tc(const bd_kv_problem* probs, int count, int dtype, int* flag, cudaS
   }
   prm.total_tiles = total;
   if (total == 0) return BD_OK;
+  static const int debug = [] {
+    const char* e = getenv("BD_TC_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  prm.debug = debug;
 
   auto kern = bf16 ? kv_proj_tc_kernel<true> : kv_proj_tc_kernel<false>;
   static bool attr_set[2] = {false, false};

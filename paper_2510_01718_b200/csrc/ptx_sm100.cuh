@@ -51,15 +51,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
-// Blocks until the phase with the given parity has completed.
+// Blocks until the phase with the given parity has completed.  No suspend-time hint:
+// with one the probe compiles to TRYWAIT + NANOSLEEP and a waiter can oversleep.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "BD_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra BD_WAIT_%=;\n\t}" ::"r"(addr),
-      "r"(parity), "r"(0x989680)
+      "r"(parity)
       : "memory");
 }
 
