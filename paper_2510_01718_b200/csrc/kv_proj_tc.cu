@@ -37,24 +37,33 @@
 namespace bdk {
 namespace tc {
 
-constexpr int BM = 128;                       // UMMA M (rows of x per tile)
+constexpr int BM = 128;                       // rows of x per CTA per tile (TMEM lanes)
 constexpr int BN = 256;                       // UMMA N (output columns per tile)
 constexpr int BK = 64;                        // k-block: one 128-byte swizzle row of A
 constexpr int UK = 16;                        // UMMA K for kind::f16
-constexpr int STAGES = 3;                     // smem ring depth (A+B)
 constexpr int EPI_WARPS = 8;                  // 2 per SMSP; warps w, w+4 share a TMEM lane quadrant
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr uint32_t A_BYTES = BM * BK * 2;     // 16 KiB
-constexpr uint32_t B_CHUNK = 64 * BK * 2;     // one 64-column MN-major swizzle panel, 8 KiB
-constexpr uint32_t B_BYTES = BN * BK * 2;     // 32 KiB
-constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr uint32_t B_PANEL = 64 * BK * 2;     // one 64-column MN-major swizzle panel, 8 KiB
 constexpr uint32_t REP_BOX = 64 * BM * 2;     // one 64-column x 128-row rep box, 16 KiB
 constexpr uint32_t REP_BYTES = 2 * REP_BOX;   // d_h <= 128 -> at most two boxes
-constexpr uint32_t STG_BYTES = 32 * 32 * 2;   // per-warp output staging: 32 rows x 32 cols (SW64)
+constexpr uint32_t STG_BYTES = 32 * 32 * 2;   // output staging box: 32 rows x 32 cols (SW64)
 constexpr uint32_t TMEM_COLS = 2 * BN;        // double-buffered accumulator
-constexpr size_t SMEM_BYTES =
-    1024 + STAGES * STAGE_BYTES + 2 * REP_BYTES + EPI_WARPS * STG_BYTES + 256;
-static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+
+// Per cta_group configuration.  CG = 2: a CTA pair computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 — each CTA stages its own 128 rows of A and HALF of the B
+// tile (128 columns), so B bytes per CTA halve and the ring can be one stage deeper.
+template <int CG>
+struct Cfg {
+  static constexpr int B_PANELS = (BN / 64) / CG;               // 4 (CG=1) / 2 (CG=2)
+  static constexpr uint32_t B_BYTES = B_PANELS * B_PANEL;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;    // 48 / 32 KiB
+  static constexpr int STAGES = CG == 1 ? 3 : 4;
+  static constexpr int STG_BUFS = CG == 1 ? 1 : 2;               // per-warp staging buffers
+  static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 2 * REP_BYTES +
+                                       EPI_WARPS * STG_BUFS * STG_BYTES + 256;
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+};
 
 struct TcProblem {
   CUtensorMap map_a;    // x + mul_base, dims {K, L},   box {64, 128}
@@ -71,18 +80,19 @@ struct TcProblem {
 struct TcParams {
   TcProblem p[BD_MAX_GROUP];
   int32_t count;
-  int32_t total_tiles;
+  int32_t total_tiles;  // tiles of (BM * CG) rows x BN columns
   int* flag;
   int32_t debug;  // profiling knob (env BD_TC_DEBUG): 1 no stores, 2 no epilogue math, 4 no LDTM
 };
 
+template <int CG>
 __device__ __forceinline__ void decode_tile(const TcParams& prm, int t, int& pi, int& m0,
                                             int& n0) {
   pi = 0;
   while (pi + 1 < prm.count && t >= prm.p[pi + 1].tile_start) ++pi;
   const int local = t - prm.p[pi].tile_start;
   n0 = (local % prm.p[pi].tiles_n) * BN;
-  m0 = (local / prm.p[pi].tiles_n) * BM;
+  m0 = (local / prm.p[pi].tiles_n) * (BM * CG);
 }
 
 // Tiles sharing (problem, m-block) share the rep tile x[m0:m0+128, rep_base:+d_h].
@@ -117,19 +127,20 @@ __device__ __forceinline__ float fmax_nan(float a, float b) {
   return r;
 }
 
-template <bool kBF16>
+template <bool kBF16, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     kv_proj_tc_kernel(const __grid_constant__ TcParams prm) {
+  using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = sA + STAGES * A_BYTES;
-  uint8_t* sRep = sB + STAGES * B_BYTES;            // 2 slots x REP_BYTES
-  uint8_t* sStg = sRep + 2 * REP_BYTES;             // EPI_WARPS x STG_BYTES
-  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + EPI_WARPS * STG_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* sB = sA + C::STAGES * A_BYTES;
+  uint8_t* sRep = sB + C::STAGES * C::B_BYTES;      // 2 slots x REP_BYTES
+  uint8_t* sStg = sRep + 2 * REP_BYTES;             // EPI_WARPS x STG_BUFS x STG_BYTES
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + EPI_WARPS * C::STG_BUFS * STG_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* rfull = tempty + 2;
   uint64_t* rempty = rfull + 2;
@@ -137,10 +148,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  // Contiguous tile range per CTA: consecutive tiles share the x row-block (A and the
-  // rep slice stay L2/smem-hot); the split is balanced to within one tile.
-  const int t_begin = static_cast<int>(static_cast<int64_t>(blockIdx.x) * prm.total_tiles / gridDim.x);
-  const int t_end = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * prm.total_tiles / gridDim.x);
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;  // 0 = pair leader
+  const int unit = CG == 2 ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int units = CG == 2 ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  // Contiguous tile range per CTA (pair): consecutive tiles share the x row-block (A and
+  // the rep slice stay L2/smem-hot); the split is balanced to within one tile.
+  const int t_begin = static_cast<int>(static_cast<int64_t>(unit) * prm.total_tiles / units);
+  const int t_end = static_cast<int>(static_cast<int64_t>(unit + 1) * prm.total_tiles / units);
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < prm.count; ++i) {
@@ -149,24 +163,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tma_prefetch_desc(&prm.p[i].map_out);
       if (prm.p[i].rep_fast) tma_prefetch_desc(&prm.p[i].map_rep);
     }
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);    // armed by the leader's producer with the pair's bytes
+      mbar_init(&empty[s], 1);   // one (multicast) tcgen05.commit
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 1);
+      mbar_init(&tempty[a], CG);  // one arrival per CTA's epilogue (leader's copy)
       mbar_init(&rfull[a], 1);
       mbar_init(&rempty[a], 1);
     }
     fence_mbar_init();
   }
   if (warp == 1) {
-    tmem_alloc(tmem_slot, TMEM_COLS);
-    tmem_relinquish();
+    tmem_alloc<CG>(tmem_slot, TMEM_COLS);
+    tmem_relinquish<CG>();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -181,9 +195,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int prev_key = -1;
       for (int t = t_begin; t < t_end; ++t) {
         int pi, m0, n0;
-        decode_tile(prm, t, pi, m0, n0);
+        decode_tile<CG>(prm, t, pi, m0, n0);
         const TcProblem& P = prm.p[pi];
-        const int key = rep_key(pi, m0);
+        const int my_m0 = m0 + static_cast<int>(rank) * BM;
+        const int my_n0 = n0 + static_cast<int>(rank) * (BN / CG);
+        const int key = rep_key(pi, my_m0);
         if (P.rep_fast && key != prev_key) {
           // New (problem, m-block): stage its rep tile in the other slot.
           rslot ^= 1;
@@ -192,20 +208,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int nbox = P.d_h / 64;
           mbar_arrive_expect_tx(&rfull[rslot], nbox * REP_BOX);
           for (int b = 0; b < nbox; ++b)
-            tma_load_2d(sRep + rslot * REP_BYTES + b * REP_BOX, &P.map_rep, 64 * b, m0,
+            tma_load_2d(sRep + rslot * REP_BYTES + b * REP_BOX, &P.map_rep, 64 * b, my_m0,
                         &rfull[rslot], pol);
         }
         prev_key = key;
         for (int kb = 0; kb < P.num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(sA + stage * A_BYTES, &P.map_a, kb * BK, m0, &full[stage], pol);
+          uint8_t* a_dst = sA + stage * A_BYTES;
+          uint8_t* b_dst = sB + stage * C::B_BYTES;
+          if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(a_dst, &P.map_a, kb * BK, my_m0, &full[stage], pol);
 #pragma unroll
-          for (int q = 0; q < BN / 64; ++q) {
-            tma_load_2d(sB + stage * B_BYTES + q * B_CHUNK, &P.map_b, n0 + 64 * q, kb * BK,
-                        &full[stage], pol);
+            for (int q = 0; q < C::B_PANELS; ++q)
+              tma_load_2d(b_dst + q * B_PANEL, &P.map_b, my_n0 + 64 * q, kb * BK, &full[stage],
+                          pol);
+          } else {
+            // Both CTAs' bytes complete on the LEADER's full barrier, which the leader
+            // arms with the pair's total.  The peer does not arrive: a cluster-scope
+            // release arrive would stall it on its own in-flight TMA loads, and the
+            // barrier cannot complete before the leader's arrival anyway.
+            const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
+            tma_load_2d_pair(a_dst, &P.map_a, kb * BK, my_m0, bar, pol);
+#pragma unroll
+            for (int q = 0; q < C::B_PANELS; ++q)
+              tma_load_2d_pair(b_dst + q * B_PANEL, &P.map_b, my_n0 + 64 * q, kb * BK, bar, pol);
           }
-          if (++stage == STAGES) {
+          if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -213,15 +243,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_f16(kBF16, BM, BN, /*a_mn=*/false, /*b_mn=*/true);
+    // ------------------------------------------------------------ MMA issuer (leader)
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc =
+          make_idesc_f16(kBF16, BM * CG, BN, /*a_mn=*/false, /*b_mn=*/true);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int t = t_begin; t < t_end; ++t, ++it) {
         int pi, m0, n0;
-        decode_tile(prm, t, pi, m0, n0);
+        decode_tile<CG>(prm, t, pi, m0, n0);
         const TcProblem& P = prm.p[pi];
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
@@ -232,24 +263,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int ks = 0; ks < BK / UK; ++ks) {
             // A: K-major SW128, rows 128 B apart, 8-row groups 1024 B apart; a 16-wide
             //    k step is +32 B inside the swizzle row.
             const uint64_t adesc = make_smem_desc(a0 + ks * (UK * 2), 16, 1024);
-            // B: MN-major SW128, 64-column panels B_CHUNK apart (LBO), 8-k-row groups
+            // B: MN-major SW128, 64-column panels B_PANEL apart (LBO), 8-k-row groups
             //    1024 B apart (SBO); a 16-deep k step is two 8-row groups = 2048 B.
-            const uint64_t bdesc = make_smem_desc(b0 + ks * (UK * 128), B_CHUNK, 1024);
-            tc_mma_f16(d_tmem, adesc, bdesc, idesc, (kb | ks) != 0 ? 1u : 0u);
+            const uint64_t bdesc = make_smem_desc(b0 + ks * (UK * 128), B_PANEL, 1024);
+            if constexpr (CG == 1)
+              tc_mma_f16(d_tmem, adesc, bdesc, idesc, (kb | ks) != 0 ? 1u : 0u);
+            else
+              tc_mma_f16_pair(d_tmem, adesc, bdesc, idesc, (kb | ks) != 0 ? 1u : 0u);
           }
-          tc_commit(&empty[stage]);
-          if (++stage == STAGES) {
+          if constexpr (CG == 1) tc_commit(&empty[stage]); else tc_commit_pair(&empty[stage], 0x3);
+          if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);
+        if constexpr (CG == 1) tc_commit(&tfull[acc]); else tc_commit_pair(&tfull[acc], 0x3);
       }
     }
   } else {
@@ -263,10 +297,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int row_w = static_cast<int>(lane);
     const int row_t = static_cast<int>(quad * 32) + row_w;
     const bool leader = (ew == 0 && lane == 0);
-    uint8_t* stg = sStg + ew * STG_BYTES;
-    const uint32_t stg_u32 = smem_u32(stg);
-    const uint32_t stg_row = stg_u32 + row_w * 64;
+    const uint32_t stg0 = smem_u32(sStg + ew * C::STG_BUFS * STG_BYTES);
     const uint32_t sw64 = static_cast<uint32_t>((row_w >> 1) & 3);
+    const uint32_t tempty_leader0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+    const uint32_t tempty_leader1 = CG == 2 ? mapa_shared(smem_u32(&tempty[1]), 0) : 0u;
+    uint32_t sbuf = 0;
     float amax = 0.f;  // NaN-propagating max |out| for the non-finite check
     int rslot = 1;
     uint32_t rphase = 0;  // bit s = parity of rep slot s
@@ -274,9 +309,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int it = 0;
     for (int t = t_begin; t < t_end; ++t, ++it) {
       int pi, m0, n0;
-      decode_tile(prm, t, pi, m0, n0);
+      decode_tile<CG>(prm, t, pi, m0, n0);
       const TcProblem& P = prm.p[pi];
-      const int key = rep_key(pi, m0);
+      const int my_m0 = m0 + static_cast<int>(rank) * BM;
+      const int key = rep_key(pi, my_m0);
       const bool fast = P.rep_fast != 0;
       if (fast && key != prev_key) {
         rslot ^= 1;
@@ -289,7 +325,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t grow = static_cast<int64_t>(m0) + row_t;
+      const int64_t grow = static_cast<int64_t>(my_m0) + row_t;
       const uint16_t* xrow = static_cast<const uint16_t*>(P.x) +
                              (grow < P.L ? grow : 0) * P.ldx + P.rep_base;
       const int cbase = n0 + static_cast<int>(half) * 128;
@@ -319,7 +355,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         : make_uint4(0, 0, 0, 0);
           }
         }
-        if (lane == 0) tma_store_wait_read<0>();  // staging free again
+        const uint32_t stg = stg0 + sbuf * STG_BYTES;
+        // the TMA store that last read this staging buffer must be done with it
+        if (lane == 0) tma_store_wait_read<C::STG_BUFS - 1>();
         __syncwarp();
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
@@ -334,7 +372,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             amax = fmax_nan(amax, fabsf(v1));
             o[e] = pack2<kBF16>(v0, v1);
           }
-          const uint32_t dst = stg_row + ((static_cast<uint32_t>(g) ^ sw64) << 4);
+          const uint32_t dst = stg + row_w * 64 + ((static_cast<uint32_t>(g) ^ sw64) << 4);
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(o[0]),
                        "r"(o[1]), "r"(o[2]), "r"(o[3])
                        : "memory");
@@ -342,9 +380,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0 && !(prm.debug & 1)) {
-          tma_store_2d(&P.map_out, stg, col0, m0 + static_cast<int>(quad) * 32);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                  reinterpret_cast<uint64_t>(&P.map_out)),
+              "r"(stg), "r"(col0), "r"(my_m0 + static_cast<int>(quad) * 32)
+              : "memory");
           tma_store_commit();
         }
+        if constexpr (C::STG_BUFS > 1) sbuf ^= 1;
       };
 
       if (!(prm.debug & 4) && nsub > 0) {
@@ -368,11 +411,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_before();
       named_bar_sync(1, 32 * EPI_WARPS);  // all epilogue threads finished with TMEM + rep
       if (leader) {
-        mbar_arrive(&tempty[acc]);
+        if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+        else mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
         if (fast) {
           int npi = -1, nm0 = 0, nn0 = 0;
-          if (t + 1 < t_end) decode_tile(prm, t + 1, npi, nm0, nn0);
-          if (t + 1 >= t_end || rep_key(npi, nm0) != key) mbar_arrive(&rempty[rslot]);
+          if (t + 1 < t_end) decode_tile<CG>(prm, t + 1, npi, nm0, nn0);
+          if (t + 1 >= t_end || rep_key(npi, nm0 + static_cast<int>(rank) * BM) != key)
+            mbar_arrive(&rempty[rslot]);
         }
       }
     }
@@ -384,10 +429,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    tmem_dealloc<CG>(tmem_base, TMEM_COLS);
   }
 }
 
@@ -436,10 +481,20 @@ bool encode_2d(CUtensorMap* map, const void* base, bool bf16, uint64_t cols, uin
 
 int launch_tc(const bd_kv_problem* probs, int count, int dtype, int* flag, cudaStream_t stream) {
   using namespace tc;
+  static const int debug = [] {
+    const char* e = getenv("BD_TC_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  // cta_group: 2 (CTA pairs) by default; BD_TC_CTA_GROUP=1 selects the single-CTA kernel.
+  static const int cg = [] {
+    const char* e = getenv("BD_TC_CTA_GROUP");
+    return (e && atoi(e) == 1) ? 1 : 2;
+  }();
   const bool bf16 = dtype == BD_BF16;
   TcParams prm{};
   prm.count = count;
   prm.flag = flag;
+  prm.debug = debug;
   int total = 0;
   for (int i = 0; i < count; ++i) {
     const bd_kv_problem& q = probs[i];
@@ -468,31 +523,48 @@ int launch_tc(const bd_kv_problem* probs, int count, int dtype, int* flag, cudaS
     P.tiles_n = static_cast<int32_t>((N + BN - 1) / BN);
     P.num_kb = static_cast<int32_t>((K + BK - 1) / BK);
     P.tile_start = total;
-    total += P.tiles_n * static_cast<int32_t>((q.L + BM - 1) / BM);
+    total += P.tiles_n * static_cast<int32_t>((q.L + BM * cg - 1) / (BM * cg));
   }
   prm.total_tiles = total;
   if (total == 0) return BD_OK;
-  static const int debug = [] {
-    const char* e = getenv("BD_TC_DEBUG");
-    return e ? atoi(e) : 0;
-  }();
-  prm.debug = debug;
 
-  auto kern = bf16 ? kv_proj_tc_kernel<true> : kv_proj_tc_kernel<false>;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[bf16 ? 1 : 0]) {
+  using KernFn = void (*)(TcParams);
+  KernFn kern;
+  size_t smem;
+  if (cg == 2) {
+    kern = bf16 ? kv_proj_tc_kernel<true, 2> : kv_proj_tc_kernel<false, 2>;
+    smem = Cfg<2>::SMEM_BYTES;
+  } else {
+    kern = bf16 ? kv_proj_tc_kernel<true, 1> : kv_proj_tc_kernel<false, 1>;
+    smem = Cfg<1>::SMEM_BYTES;
+  }
+  static bool attr_set[2][2] = {{false, false}, {false, false}};
+  if (!attr_set[cg - 1][bf16 ? 1 : 0]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(SMEM_BYTES));
+                                         static_cast<int>(smem));
     if (e != cudaSuccess) {
       set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
       return BD_ERR_CUDA;
     }
-    attr_set[bf16 ? 1 : 0] = true;
+    attr_set[cg - 1][bf16 ? 1 : 0] = true;
   }
-  const int grid = total < sm_count() ? total : sm_count();
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(prm);
+  const int units = sm_count() / cg;
+  const int grid_units = total < units ? total : units;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid_units * cg);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cg;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm);
   note_launch();
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("kv_proj_tc launch: ") + cudaGetErrorString(e));
     return BD_ERR_CUDA;
