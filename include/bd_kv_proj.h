@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define BD_KV_PROJ_ABI_VERSION 1
+#define BD_KV_PROJ_ABI_VERSION 2
 
 /* element types */
 enum bd_dtype { BD_F32 = 0, BD_F64 = 1, BD_F16 = 2, BD_BF16 = 3 };
@@ -109,6 +109,30 @@ int bd_kv_proj_grouped(const bd_kv_problem* problems, int count, int dtype, int 
 int bd_kv_proj_host(const void* x, const void* c, void* out, int64_t L, int64_t d, int64_t d_h,
                     int64_t n_heads, int64_t mul_base, int64_t rep_base, int dtype, int mode,
                     int* nonfinite);
+
+/*
+ * Plain product out = a @ b on device buffers (a: M x K, b: K x N, out: M x N, row-major
+ * with row strides lda/ldb/ldo), stream-ordered.  F32/F64 run the exact kernel and are
+ * bit-identical to the reference's fixed-order matmul; F16/BF16 run the tensor-core
+ * kernel without the repeated-slice add.
+ * Replaces: bdattn.matmul / _matmul_kernel (ref: pkg/src/bdattn/tensor.py:189-213).
+ */
+int bd_matmul(const void* a, int64_t lda, const void* b, int64_t ldb, void* out, int64_t ldo,
+              int64_t M, int64_t K, int64_t N, int dtype, int mode, int* nonfinite_flag,
+              void* stream);
+
+/*
+ * BD low-rank linear layer forward on device buffers: h = x @ basis (L x rank), then
+ * y = [h, h @ coeff] for tag FIRST or [h @ coeff, h] for LAST (y: L x d_out, stride ldy).
+ * h is written straight into its final columns of y and read back from there as the
+ * second product's A operand (no concat buffer).  Two launches on `stream`.
+ * basis: d_in x rank (ldb), coeff: rank x (d_out - rank) (ldc).
+ * Replaces: bdattn.bd_linear_forward (ref: pkg/src/bdattn/linear.py:101-108).
+ */
+int bd_linear_forward(const void* x, int64_t ldx, const void* basis, int64_t ldb,
+                      const void* coeff, int64_t ldc, void* y, int64_t ldy, int64_t L,
+                      int64_t d_in, int64_t rank, int64_t d_out, int tag, int dtype, int mode,
+                      int* nonfinite_flag, void* stream);
 
 /* Human-readable description of the last error on this thread ("" if none). */
 const char* bd_last_error(void);

@@ -8,23 +8,29 @@ when the library is missing — there is no CPU fallback on the product path.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 from .errors import NativeLibraryError, PrecisionError, ShapeError
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbd_kvproj.so"
+if os.environ.get("BD_LIB_PATH"):  # development aid: load an experimental build
+    LIB_PATH = Path(os.environ["BD_LIB_PATH"])
 
 # enum bd_dtype / bd_status / bd_mode / bd_tag  (include/bd_kv_proj.h)
 BD_F32, BD_F64, BD_F16, BD_BF16 = 0, 1, 2, 3
 BD_OK, BD_ERR_SHAPE, BD_ERR_DTYPE, BD_ERR_ALIGN, BD_ERR_CUDA, BD_ERR_ARG = 0, 1, 2, 3, 4, 5
 BD_MODE_AUTO, BD_MODE_EXACT, BD_MODE_TC = 0, 1, 2
 BD_MAX_GROUP = 4
-ABI_VERSION = 1
+ABI_VERSION = 2
+BD_TAG_FIRST, BD_TAG_LAST = 0, 1
 
 EXPORTED_SYMBOLS = (
     "bd_kv_proj",
     "bd_kv_proj_grouped",
     "bd_kv_proj_host",
+    "bd_matmul",
+    "bd_linear_forward",
     "bd_last_error",
     "bd_abi_version",
     "bd_launch_count",
@@ -75,6 +81,11 @@ def load() -> ctypes.CDLL:
     lib.bd_kv_proj_host.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, ci, ci,
                                     ctypes.POINTER(ctypes.c_int)]
     lib.bd_kv_proj_host.restype = ci
+    lib.bd_matmul.argtypes = [vp, i64, vp, i64, vp, i64, i64, i64, i64, ci, ci, vp, vp]
+    lib.bd_matmul.restype = ci
+    lib.bd_linear_forward.argtypes = [vp, i64, vp, i64, vp, i64, vp, i64, i64, i64, i64, i64, ci,
+                                      ci, ci, vp, vp]
+    lib.bd_linear_forward.restype = ci
     lib.bd_last_error.argtypes = []
     lib.bd_last_error.restype = ctypes.c_char_p
     lib.bd_abi_version.argtypes = []

@@ -104,6 +104,22 @@ int validate(const bd_kv_problem& p, int dtype, int mode, int idx) {
   return BD_OK;
 }
 
+Problem to_problem(const bd_kv_problem& q) {
+  return Problem{q.x, q.c, q.out, q.ldx, q.ldc, q.ldo, q.L, q.d - q.d_h, q.n_heads * q.d_h,
+                 q.d_h, q.mul_base, q.rep_base};
+}
+
+int dispatch(const Problem* probs, int count, int dtype, int m, int* flag, cudaStream_t stream) {
+  g_last_error.clear();
+  if (m == BD_MODE_EXACT) {
+    cudaError_t e = launch_exact(probs, count, dtype, flag, stream);
+    if (e != cudaSuccess)
+      return fail(BD_ERR_CUDA, std::string("kv_proj_exact: ") + cudaGetErrorString(e));
+    return BD_OK;
+  }
+  return launch_tc(probs, count, dtype, flag, stream);
+}
+
 int run_group(const bd_kv_problem* probs, int count, int dtype, int mode, int* flag,
               cudaStream_t stream) {
   if (probs == nullptr || count < 1 || count > BD_MAX_GROUP)
@@ -112,17 +128,41 @@ int run_group(const bd_kv_problem* probs, int count, int dtype, int mode, int* f
   int m = 0;
   int rc = resolve_mode(dtype, mode, &m);
   if (rc != BD_OK) return rc;
+  Problem ps[BD_MAX_GROUP];
   for (int i = 0; i < count; ++i) {
     rc = validate(probs[i], dtype, m, i);
     if (rc != BD_OK) return rc;
+    ps[i] = to_problem(probs[i]);
   }
-  g_last_error.clear();
-  if (m == BD_MODE_EXACT) {
-    cudaError_t e = launch_exact(probs, count, dtype, flag, stream);
-    if (e != cudaSuccess) return fail(BD_ERR_CUDA, std::string("kv_proj_exact: ") + cudaGetErrorString(e));
-    return BD_OK;
+  return dispatch(ps, count, dtype, m, flag, stream);
+}
+
+// A plain product (no repeated-slice add): validation for raw pointers/strides.
+int validate_matmul(const void* a, int64_t lda, const void* b, int64_t ldb, const void* out,
+                    int64_t ldo, int64_t M, int64_t K, int64_t N, int m, const char* what) {
+  char buf[256];
+  if (a == nullptr || b == nullptr || out == nullptr)
+    return fail(BD_ERR_ARG, std::string(what) + ": null pointer");
+  if (M < 1 || K < 1 || N < 1) {
+    snprintf(buf, sizeof(buf), "%s: non-positive size (M=%lld K=%lld N=%lld)", what,
+             (long long)M, (long long)K, (long long)N);
+    return fail(BD_ERR_SHAPE, buf);
   }
-  return launch_tc(probs, count, dtype, flag, stream);
+  if (lda < K || ldb < N || ldo < N) {
+    snprintf(buf, sizeof(buf), "%s: row strides too small (lda=%lld ldb=%lld ldo=%lld)", what,
+             (long long)lda, (long long)ldb, (long long)ldo);
+    return fail(BD_ERR_SHAPE, buf);
+  }
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
+    return fail(BD_ERR_SHAPE, std::string(what) + ": dimension exceeds int32 range");
+  if (m == BD_MODE_TC) {
+    if (!aligned16(a) || !aligned16(b) || !aligned16(out))
+      return fail(BD_ERR_ALIGN, std::string(what) + ": tensor-core path needs 16-byte aligned operands");
+    if ((lda | ldb | ldo | K | N) & 7)
+      return fail(BD_ERR_ALIGN, std::string(what) +
+                                    ": tensor-core path needs lda, ldb, ldo, K and N to be multiples of 8");
+  }
+  return BD_OK;
 }
 
 // Per-thread device staging for the synchronous host entry point.
@@ -214,7 +254,7 @@ int bd_kv_proj_host(const void* x, const void* c, void* out, int64_t L, int64_t 
   if (e == cudaSuccess) e = cudaMemcpyAsync(dx, x, static_cast<size_t>(L * d) * es, cudaMemcpyHostToDevice, s.stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dc, c, static_cast<size_t>(K * N) * es, cudaMemcpyHostToDevice, s.stream);
   if (e != cudaSuccess) return fail(BD_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e));
-  bd_kv_problem p{dx, dc, dout, d, N, N, L, d, d_h, n_heads, mul_base, rep_base};
+  bd_kv_problem p{dx, dc, dout, d, N, N, L, d, d_h, n_heads, mul_base, rep_base};  // device copies
   int rc = run_group(&p, 1, dtype, mode, s.flag, s.stream);
   if (rc != BD_OK) {
     cudaStreamSynchronize(s.stream);
@@ -227,6 +267,55 @@ int bd_kv_proj_host(const void* x, const void* c, void* out, int64_t L, int64_t 
   if (e != cudaSuccess) return fail(BD_ERR_CUDA, std::string("D2H: ") + cudaGetErrorString(e));
   if (nonfinite) *nonfinite = hflag;
   return BD_OK;
+}
+
+int bd_matmul(const void* a, int64_t lda, const void* b, int64_t ldb, void* out, int64_t ldo,
+              int64_t M, int64_t K, int64_t N, int dtype, int mode, int* nonfinite_flag,
+              void* stream) {
+  using namespace bdk;
+  if (elem_size(dtype) == 0) return fail(BD_ERR_DTYPE, "unknown dtype " + std::to_string(dtype));
+  int m = 0;
+  int rc = resolve_mode(dtype, mode, &m);
+  if (rc != BD_OK) return rc;
+  rc = validate_matmul(a, lda, b, ldb, out, ldo, M, K, N, m, "bd_matmul");
+  if (rc != BD_OK) return rc;
+  Problem p{a, b, out, lda, ldb, ldo, M, K, N, 1, 0, -1};
+  return dispatch(&p, 1, dtype, m, nonfinite_flag, static_cast<cudaStream_t>(stream));
+}
+
+int bd_linear_forward(const void* x, int64_t ldx, const void* basis, int64_t ldb,
+                      const void* coeff, int64_t ldc, void* y, int64_t ldy, int64_t L,
+                      int64_t d_in, int64_t rank, int64_t d_out, int tag, int dtype, int mode,
+                      int* nonfinite_flag, void* stream) {
+  using namespace bdk;
+  const size_t es = elem_size(dtype);
+  if (es == 0) return fail(BD_ERR_DTYPE, "unknown dtype " + std::to_string(dtype));
+  if (tag != BD_TAG_FIRST && tag != BD_TAG_LAST)
+    return fail(BD_ERR_ARG, "unknown tag " + std::to_string(tag));
+  if (rank < 1 || rank >= d_out || rank > d_in)
+    return fail(BD_ERR_SHAPE, "rank must satisfy 1 <= rank < d_out and rank <= d_in");
+  if (ldy < d_out) return fail(BD_ERR_SHAPE, "ldy < d_out");
+  int m = 0;
+  int rc = resolve_mode(dtype, mode, &m);
+  if (rc != BD_OK) return rc;
+  // y = [h, h C] (FIRST) or [h C, h] (LAST): h lands in its final columns and is read
+  // back from there as the second product's A operand, so no concat is materialised.
+  const int64_t h_off = tag == BD_TAG_FIRST ? 0 : d_out - rank;
+  const int64_t hc_off = tag == BD_TAG_FIRST ? rank : 0;
+  char* yb = static_cast<char*>(y);
+  void* h = yb + h_off * static_cast<int64_t>(es);
+  void* hc = yb + hc_off * static_cast<int64_t>(es);
+  rc = validate_matmul(x, ldx, basis, ldb, h, ldy, L, d_in, rank, m, "bd_linear_forward h = x B");
+  if (rc != BD_OK) return rc;
+  rc = validate_matmul(h, ldy, coeff, ldc, hc, ldy, L, rank, d_out - rank, m,
+                       "bd_linear_forward h C");
+  if (rc != BD_OK) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Problem p1{x, basis, h, ldx, ldb, ldy, L, d_in, rank, 1, 0, -1};
+  rc = dispatch(&p1, 1, dtype, m, nonfinite_flag, s);
+  if (rc != BD_OK) return rc;
+  Problem p2{h, coeff, hc, ldy, ldc, ldy, L, rank, d_out - rank, 1, 0, -1};
+  return dispatch(&p2, 1, dtype, m, nonfinite_flag, s);
 }
 
 const char* bd_last_error(void) { return bdk::g_last_error.c_str(); }

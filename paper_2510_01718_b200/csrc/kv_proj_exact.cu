@@ -40,7 +40,7 @@ struct ExactOps<double> {
 };
 
 struct ExactGroup {
-  bd_kv_problem p[BD_MAX_GROUP];
+  Problem p[BD_MAX_GROUP];
   int tiles_n[BD_MAX_GROUP];
   int tile_start[BD_MAX_GROUP + 1];
   int count;
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(EX_THREADS)
   int t = blockIdx.x;
   int pi = 0;
   while (pi + 1 < g.count && t >= g.tile_start[pi + 1]) ++pi;
-  const bd_kv_problem& P = g.p[pi];
+  const Problem& P = g.p[pi];
   const int local = t - g.tile_start[pi];
   const int tn = local % g.tiles_n[pi];
   const int tm = local / g.tiles_n[pi];
@@ -63,8 +63,8 @@ __global__ void __launch_bounds__(EX_THREADS)
   const T* __restrict__ x = static_cast<const T*>(P.x);
   const T* __restrict__ c = static_cast<const T*>(P.c);
   T* __restrict__ out = static_cast<T*>(P.out);
-  const int64_t K = P.d - P.d_h;
-  const int64_t N = P.n_heads * P.d_h;
+  const int64_t K = P.K;
+  const int64_t N = P.N;
 
   __shared__ T xs[EX_BK][EX_BM];  // x slab, k-major so a thread's 4 rows are contiguous
   __shared__ T cs[EX_BK][EX_BN];
@@ -108,6 +108,9 @@ __global__ void __launch_bounds__(EX_THREADS)
   }
 
   // Epilogue: + the repeated basis slice, after the full sum (attention.py:266-270).
+  // Without it (rep_base < 0) this is the reference's fixed-order matmul
+  // (tensor.py:189-213), used by the BD low-rank layer.
+  const bool has_rep = P.rep_base >= 0;
   bool bad = false;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -117,8 +120,8 @@ __global__ void __launch_bounds__(EX_THREADS)
     for (int j = 0; j < 4; ++j) {
       const int64_t col = n0 + tx * 4 + j;
       if (col >= N) continue;
-      const T rep = x[row * P.ldx + P.rep_base + (col % P.d_h)];
-      const T v = ExactOps<T>::add(acc[i][j], rep);
+      const T v = has_rep ? ExactOps<T>::add(acc[i][j], x[row * P.ldx + P.rep_base + (col % P.d_h)])
+                          : acc[i][j];
       out[row * P.ldo + col] = v;
       bad |= !isfinite(v);
     }
@@ -130,14 +133,14 @@ __global__ void __launch_bounds__(EX_THREADS)
 
 }  // namespace
 
-cudaError_t launch_exact(const bd_kv_problem* probs, int count, int dtype, int* flag,
+cudaError_t launch_exact(const Problem* probs, int count, int dtype, int* flag,
                          cudaStream_t stream) {
   ExactGroup g{};
   g.count = count;
   int total = 0;
   for (int i = 0; i < count; ++i) {
     g.p[i] = probs[i];
-    const int64_t N = probs[i].n_heads * probs[i].d_h;
+    const int64_t N = probs[i].N;
     const int64_t tn = (N + EX_BN - 1) / EX_BN;
     const int64_t tm = (probs[i].L + EX_BM - 1) / EX_BM;
     g.tiles_n[i] = static_cast<int>(tn);

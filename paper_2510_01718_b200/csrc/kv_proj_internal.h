@@ -9,6 +9,21 @@
 
 namespace bdk {
 
+// One contraction as the kernels see it:
+//   out[i, j] = sum_{k<K} x[i, mul_base + k] * c[k, j]   (+ x[i, rep_base + j % d_h])
+// The BD projection is K = d - d_h, N = n_heads * d_h with the repeated-slice add; a
+// plain GEMM (the BD low-rank layer's two products) sets rep_base < 0 (no add).
+struct Problem {
+  const void* x;
+  const void* c;
+  void* out;
+  int64_t ldx, ldc, ldo;
+  int64_t L, K, N;
+  int64_t d_h;       // head width of the repeated slice (ignored without rep)
+  int64_t mul_base;  // first multiplied column of x
+  int64_t rep_base;  // first repeated column of x; < 0: no repeated-slice add
+};
+
 // Thread-local error text set by the launchers; returned by bd_last_error().
 void set_error(const std::string& msg);
 
@@ -16,11 +31,11 @@ void set_error(const std::string& msg);
 void note_launch();
 
 // Exact SIMT kernel (FP32/FP64): reference rounding sequence (attention.py:258-270).
-cudaError_t launch_exact(const bd_kv_problem* probs, int count, int dtype, int* flag,
+cudaError_t launch_exact(const Problem* probs, int count, int dtype, int* flag,
                          cudaStream_t stream);
 
 // tcgen05 tensor-core kernel (FP16/BF16). Returns BD_* status; sets error text.
-int launch_tc(const bd_kv_problem* probs, int count, int dtype, int* flag, cudaStream_t stream);
+int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_t stream);
 
 // SM count of the current device (cached).
 int sm_count();

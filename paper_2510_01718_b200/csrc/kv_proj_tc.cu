@@ -3,6 +3,7 @@
 //   out[i, h*d_h + j] = sum_k x[i, mul_base + k] * c[k, h*d_h + j]  +  x[i, rep_base + j]
 //
 // (ref: pkg/src/bdattn/attention.py:249-270 computes the same thing on the CPU.)
+// With rep_base < 0 the same kernel is a plain GEMM (the BD low-rank layer, linear.py).
 //
 // Structure (one persistent CTA per SM, warp-specialised):
 //   warp 0      TMA producer: A = x[:, mul_base : mul_base+K] as a K-major operand
@@ -74,6 +75,7 @@ struct TcProblem {
   int64_t ldx;
   int32_t L, N, K, d_h, rep_base;
   int32_t tiles_n, num_kb, tile_start;
+  int32_t has_rep;      // 0: plain GEMM (no repeated-slice add)
   int32_t rep_fast;     // d_h in {64, 128}: rep tile staged in smem by TMA
 };
 
@@ -326,6 +328,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t grow = static_cast<int64_t>(my_m0) + row_t;
+      const bool has_rep = P.has_rep != 0;
       const uint16_t* xrow = static_cast<const uint16_t*>(P.x) +
                              (grow < P.L ? grow : 0) * P.ldx + P.rep_base;
       const int cbase = n0 + static_cast<int>(half) * 128;
@@ -346,6 +349,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             xv[g] = *reinterpret_cast<const uint4*>(rep_row + (jj >> 6) * REP_BOX +
                                                     ((ch ^ (row_t & 7)) << 4));
           }
+        } else if (!has_rep) {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) xv[g] = make_uint4(0, 0, 0, 0);
         } else {
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
@@ -479,7 +485,7 @@ bool encode_2d(CUtensorMap* map, const void* base, bool bf16, uint64_t cols, uin
 
 }  // namespace tc
 
-int launch_tc(const bd_kv_problem* probs, int count, int dtype, int* flag, cudaStream_t stream) {
+int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_t stream) {
   using namespace tc;
   static const int debug = [] {
     const char* e = getenv("BD_TC_DEBUG");
@@ -497,29 +503,33 @@ int launch_tc(const bd_kv_problem* probs, int count, int dtype, int* flag, cudaS
   prm.debug = debug;
   int total = 0;
   for (int i = 0; i < count; ++i) {
-    const bd_kv_problem& q = probs[i];
+    const Problem& q = probs[i];
     TcProblem& P = prm.p[i];
-    const int64_t K = q.d - q.d_h;
-    const int64_t N = q.n_heads * q.d_h;
+    const int64_t K = q.K;
+    const int64_t N = q.N;
     std::string err;
+    const bool has_rep = q.rep_base >= 0;
+    const int64_t d_h = has_rep ? q.d_h : 1;
+    const int64_t rep_base = has_rep ? q.rep_base : 0;
     const auto* xb = static_cast<const uint16_t*>(q.x) + q.mul_base;
-    const bool rep_fast = (q.d_h % 64 == 0) && q.d_h <= 128;
-    const auto* xr = static_cast<const uint16_t*>(q.x) + q.rep_base;
+    const bool rep_fast = has_rep && (d_h % 64 == 0) && d_h <= 128;
+    const auto* xr = static_cast<const uint16_t*>(q.x) + rep_base;
     if (!encode_2d(&P.map_a, xb, bf16, K, q.L, q.ldx, BK, BM, &err) ||
         !encode_2d(&P.map_b, q.c, bf16, N, K, q.ldc, 64, BK, &err) ||
         !encode_2d(&P.map_out, q.out, bf16, N, q.L, q.ldo, 32, 32, &err, CU_TENSOR_MAP_SWIZZLE_64B) ||
-        (rep_fast && !encode_2d(&P.map_rep, xr, bf16, q.d_h, q.L, q.ldx, 64, BM, &err))) {
+        (rep_fast && !encode_2d(&P.map_rep, xr, bf16, d_h, q.L, q.ldx, 64, BM, &err))) {
       set_error(err);
       return BD_ERR_CUDA;
     }
     P.rep_fast = rep_fast ? 1 : 0;
+    P.has_rep = has_rep ? 1 : 0;
     P.x = q.x;
     P.ldx = q.ldx;
     P.L = static_cast<int32_t>(q.L);
     P.N = static_cast<int32_t>(N);
     P.K = static_cast<int32_t>(K);
-    P.d_h = static_cast<int32_t>(q.d_h);
-    P.rep_base = static_cast<int32_t>(q.rep_base);
+    P.d_h = static_cast<int32_t>(d_h);
+    P.rep_base = static_cast<int32_t>(rep_base);
     P.tiles_n = static_cast<int32_t>((N + BN - 1) / BN);
     P.num_kb = static_cast<int32_t>((K + BK - 1) / BK);
     P.tile_start = total;

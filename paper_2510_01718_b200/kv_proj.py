@@ -20,21 +20,14 @@ numba call boundary exactly.
 from __future__ import annotations
 
 import ctypes
-from enum import Enum
 from typing import Sequence
 
 import numpy as np
 import torch
 
 from . import _native as N
+from .decompose import Tag
 from .errors import NativeLibraryError, PrecisionError, ShapeError
-
-
-class Tag(Enum):
-    """Which contiguous block serves as the basis (ref: decompose.py:27-31)."""
-
-    FIRST = "first"
-    LAST = "last"
 
 
 _DTYPES = {
