@@ -1,0 +1,264 @@
+"""DeepSeek-V2-Lite MLA attention block with a BD-rewritten ``kv_b_proj`` (BASELINE
+config 5).
+
+MLA (multi-head latent attention) projects the hidden state to a shared latent
+``c_kv`` (kv_lora_rank = 512), RMS-normalises it and expands it per head with
+``kv_b_proj`` into K_nope (128) and V (128); a decoupled RoPE part (64 dims) is computed
+separately (``q_pe`` per head, ``k_pe`` shared).  Structure after transformers 5.5
+``models/deepseek_v2/modeling_deepseek_v2.py:317-359`` [ext]; geometry from
+BASELINE.json (hidden 2048, 16 heads, no q-LoRA).
+
+BD applies to the no-RoPE part exactly as to MHA:
+
+* QK, per head h: P_qk = W_q_nope^h (hidden x 128) @ W_uk^h^T (128 x 512) has rank 128;
+  its COLUMN BD picks 128 latent dims S_k: basis B_qk^h = P_qk[:, S_k] replaces the
+  head's q_nope weight and C^h (128 x 384) gives K'_h = c_kv[:, S_k] + c_kv[:, ~S_k] C^h^T.
+* VO, per head h: P_vo = W_uv^h (512 x 128) @ W_o^h (128 x hidden); its ROW BD picks S_v:
+  B_vo^h = P_vo[S_v, :] replaces the head's rows of o_proj and V'_h = c_kv[:, S_v] +
+  c_kv[:, ~S_v] C_vo^h.
+* One tag per target for all heads by mean residual (ref attention.py:181-189), so the
+  K' and V' of all heads are ONE grouped launch of the BD kernel — exactly BASELINE
+  config 2 — and kv_b_proj's 512 x 4096 weight becomes two 384 x 2048 coefficient
+  matrices (25 % fewer weights, 4/3 fewer FLOPs in that GEMM).
+* The RoPE channels are untouched: q_pe, k_pe and the 1/sqrt(192) softmax scale are
+  the same in both forms, so scores are preserved exactly (in exact arithmetic).
+
+Weights use the x @ W convention of the reference (row-major [in, out]).  Prep runs
+offline on the CPU in float64 through the same decompose path as ``bda_prepare``.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.nn.functional as F
+
+from .attention import select_tag
+from .decompose import Axis, Tag, bd_decompose_both, ordered_matmul
+from .errors import ShapeError
+from .kv_proj import fused_kv_proj_grouped
+
+
+@dataclass(frozen=True)
+class MLAConfig:
+    hidden: int = 2048
+    n_heads: int = 16
+    kv_lora_rank: int = 512
+    qk_nope: int = 128
+    qk_rope: int = 64
+    v_head: int = 128
+    rope_theta: float = 10000.0
+    rms_eps: float = 1e-6
+
+    @property
+    def qk_head(self) -> int:
+        return self.qk_nope + self.qk_rope
+
+
+DSV2_LITE = MLAConfig()
+
+
+@dataclass(frozen=True)
+class MLAWeights:
+    """Dense MLA block weights (x @ W layout)."""
+
+    cfg: MLAConfig
+    w_q: torch.Tensor      # hidden x H (nope + rope), per head [nope | rope]
+    w_kva: torch.Tensor    # hidden x (kv_lora + rope):  [c_kv | k_pe]
+    kva_norm: torch.Tensor  # kv_lora (RMSNorm weight)
+    w_kvb: torch.Tensor    # kv_lora x H (nope + v), per head [k_nope | v]
+    w_o: torch.Tensor      # H v x hidden
+
+    def to(self, device=None, dtype=None) -> "MLAWeights":
+        f = {k: getattr(self, k).to(device=device, dtype=dtype)
+             for k in ("w_q", "w_kva", "kva_norm", "w_kvb", "w_o")}
+        return replace(self, **f)
+
+
+@dataclass(frozen=True)
+class BDMLAWeights:
+    """MLA block with the BD-rewritten kv_b_proj / q_nope / o_proj."""
+
+    cfg: MLAConfig
+    w_q: torch.Tensor       # hidden x H (nope + rope): per head [B_qk^h | W_q_rope^h]
+    w_kva: torch.Tensor
+    kva_norm: torch.Tensor
+    c_qk: torch.Tensor      # (kv_lora - nope) x H nope, reference layout
+    c_vo: torch.Tensor      # (kv_lora - v) x H v
+    b_vo: torch.Tensor      # H v x hidden
+    qk_tag: Tag
+    vo_tag: Tag
+    qk_candidate_residuals: tuple[float, float]
+    vo_candidate_residuals: tuple[float, float]
+    n_heads: int            # heads held (== cfg.n_heads unless head-sharded)
+
+    def to(self, device=None, dtype=None) -> "BDMLAWeights":
+        f = {k: getattr(self, k).to(device=device, dtype=dtype)
+             for k in ("w_q", "w_kva", "kva_norm", "c_qk", "c_vo", "b_vo")}
+        return replace(self, **f)
+
+    @property
+    def kv_param_count(self) -> int:
+        return int(self.c_qk.numel() + self.c_vo.numel())
+
+
+def gen_random_mla(seed: int, cfg: MLAConfig = DSV2_LITE, dtype=torch.float64,
+                   device="cpu") -> MLAWeights:
+    """Random-init block: N(0,1)/sqrt(fan_in) weights, RMSNorm weight 1 (synthetic,
+    no checkpoint is available offline)."""
+    g = torch.Generator().manual_seed(seed)
+    H = cfg.n_heads
+
+    def w(i, o):
+        return (torch.randn(i, o, generator=g, dtype=torch.float64) / math.sqrt(i)).to(device, dtype)
+
+    return MLAWeights(cfg=cfg, w_q=w(cfg.hidden, H * cfg.qk_head),
+                      w_kva=w(cfg.hidden, cfg.kv_lora_rank + cfg.qk_rope),
+                      kva_norm=torch.ones(cfg.kv_lora_rank, dtype=dtype, device=device),
+                      w_kvb=w(cfg.kv_lora_rank, H * (cfg.qk_nope + cfg.v_head)),
+                      w_o=w(H * cfg.v_head, cfg.hidden))
+
+
+def mla_prepare(w: MLAWeights, *, force_first: bool = False) -> BDMLAWeights:
+    """Offline BD of the MLA block (float64 on the CPU, rounded to the model dtype)."""
+    cfg, H = w.cfg, w.cfg.n_heads
+    if cfg.qk_nope != cfg.v_head:
+        raise ShapeError("the grouped K'/V' launch needs qk_nope == v_head")
+    nope, rope, dv, r = cfg.qk_nope, cfg.qk_rope, cfg.v_head, cfg.kv_lora_rank
+    f64 = lambda t: np.ascontiguousarray(t.detach().to("cpu", torch.float64).numpy())  # noqa: E731
+    wq, wkvb, wo = f64(w.w_q), f64(w.w_kvb), f64(w.w_o)
+    qk_pairs, vo_pairs = [], []
+    for h in range(H):
+        q0 = h * (nope + rope)
+        k0 = h * (nope + dv)
+        w_qn = np.ascontiguousarray(wq[:, q0:q0 + nope])             # hidden x 128
+        w_uk_t = np.ascontiguousarray(wkvb[:, k0:k0 + nope].T)       # 128 x 512
+        w_uv = np.ascontiguousarray(wkvb[:, k0 + nope:k0 + nope + dv])  # 512 x 128
+        w_oh = np.ascontiguousarray(wo[h * dv:(h + 1) * dv, :])      # 128 x hidden
+        qk_pairs.append(bd_decompose_both(ordered_matmul(w_qn, w_uk_t), nope, Axis.COLUMN))
+        vo_pairs.append(bd_decompose_both(ordered_matmul(w_uv, w_oh), dv, Axis.ROW))
+    qk_tag, qk_means = select_tag(qk_pairs, force_first)
+    vo_tag, vo_means = select_tag(vo_pairs, force_first)
+    qk_sel = [p[0 if qk_tag is Tag.FIRST else 1] for p in qk_pairs]
+    vo_sel = [p[0 if vo_tag is Tag.FIRST else 1] for p in vo_pairs]
+    wq_bd = wq.copy()
+    for h, f in enumerate(qk_sel):  # B_qk^h replaces the head's q_nope weight
+        wq_bd[:, h * (nope + rope):h * (nope + rope) + nope] = f.basis
+    c_qk = np.concatenate([np.ascontiguousarray(f.coeff.T) for f in qk_sel], axis=1)
+    c_vo = np.concatenate([f.coeff for f in vo_sel], axis=1)
+    b_vo = np.concatenate([f.basis for f in vo_sel], axis=0)
+    dev, dt = w.w_q.device, w.w_q.dtype
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
+    assert c_qk.shape == (r - nope, H * nope) and b_vo.shape == (H * dv, cfg.hidden)
+    return BDMLAWeights(cfg=cfg, w_q=t(wq_bd), w_kva=w.w_kva, kva_norm=w.kva_norm, c_qk=t(c_qk),
+                        c_vo=t(c_vo), b_vo=t(b_vo), qk_tag=qk_tag, vo_tag=vo_tag,
+                        qk_candidate_residuals=qk_means, vo_candidate_residuals=vo_means,
+                        n_heads=H)
+
+
+def shard_bd_mla(w: BDMLAWeights, world: int, rank: int) -> BDMLAWeights:
+    """Heads [r H/g, (r+1) H/g): q columns, C columns, B_vo rows; w_kva replicated."""
+    from .parallel import head_range
+    cfg = w.cfg
+    h0, h1 = head_range(w.n_heads, world, rank)
+    qh, dn, dv = cfg.qk_head, cfg.qk_nope, cfg.v_head
+    return replace(w, w_q=w.w_q[:, h0 * qh:h1 * qh].contiguous(),
+                   c_qk=w.c_qk[:, h0 * dn:h1 * dn].contiguous(),
+                   c_vo=w.c_vo[:, h0 * dv:h1 * dv].contiguous(),
+                   b_vo=w.b_vo[h0 * dv:h1 * dv, :].contiguous(), n_heads=h1 - h0)
+
+
+# --------------------------------------------------------------------------- forward
+def _rms_norm(x: torch.Tensor, weight: torch.Tensor, eps: float) -> torch.Tensor:
+    xf = x.float()
+    y = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)
+    return (y * weight.float()).to(x.dtype)
+
+
+def _rope(t: torch.Tensor, theta: float) -> torch.Tensor:
+    """Rotate-half RoPE over the last dim of [L, ..., r] at positions 0..L-1."""
+    L, r = t.shape[0], t.shape[-1]
+    inv = theta ** (-torch.arange(0, r, 2, device=t.device, dtype=torch.float32) / r)
+    ang = torch.arange(L, device=t.device, dtype=torch.float32)[:, None] * inv[None, :]
+    cos = torch.cat([ang.cos(), ang.cos()], -1)
+    sin = torch.cat([ang.sin(), ang.sin()], -1)
+    shape = (L,) + (1,) * (t.dim() - 2) + (r,)
+    tf = t.float()
+    rot = torch.cat([-tf[..., r // 2:], tf[..., :r // 2]], -1)
+    return (tf * cos.view(shape) + rot * sin.view(shape)).to(t.dtype)
+
+
+def _mla_attend(q_nope, q_pe, k_nope, k_pe, v, n_heads, cfg: MLAConfig, causal=True):
+    """softmax([q_nope|q_pe][k_nope|k_pe]^T / sqrt(192)) v per head, one SDPA call."""
+    L = q_nope.shape[0]
+    q = torch.cat([q_nope.view(L, n_heads, cfg.qk_nope), q_pe.view(L, n_heads, cfg.qk_rope)], -1)
+    k = torch.cat([k_nope.view(L, n_heads, cfg.qk_nope),
+                   k_pe.view(L, 1, cfg.qk_rope).expand(L, n_heads, cfg.qk_rope)], -1)
+    vh = v.view(L, n_heads, cfg.v_head)
+    if cfg.v_head != cfg.qk_head:  # fused SDPA kernels want equal head dims: zero-pad V
+        vh = F.pad(vh, (0, cfg.qk_head - cfg.v_head))
+    o = F.scaled_dot_product_attention(q.transpose(0, 1), k.transpose(0, 1), vh.transpose(0, 1),
+                                       is_causal=causal, scale=1.0 / math.sqrt(cfg.qk_head))
+    return o.transpose(0, 1)[..., :cfg.v_head].reshape(L, n_heads * cfg.v_head)
+
+
+def _split_q(q: torch.Tensor, n_heads: int, cfg: MLAConfig):
+    L = q.shape[0]
+    qh = q.view(L, n_heads, cfg.qk_head)
+    return qh[..., :cfg.qk_nope].reshape(L, -1), qh[..., cfg.qk_nope:]
+
+
+def _latent(hidden: torch.Tensor, w_kva, kva_norm, cfg: MLAConfig):
+    kv = hidden @ w_kva
+    c_kv = _rms_norm(kv[:, :cfg.kv_lora_rank], kva_norm, cfg.rms_eps)
+    return c_kv.contiguous(), kv[:, cfg.kv_lora_rank:]
+
+
+def mla_forward(hidden: torch.Tensor, w: MLAWeights, *, causal: bool = True) -> torch.Tensor:
+    """Dense MLA block (the baseline): cuBLAS kv_b_proj with the original weight."""
+    cfg, H = w.cfg, w.cfg.n_heads
+    q_nope, q_pe = _split_q(hidden @ w.w_q, H, cfg)
+    c_kv, k_pe = _latent(hidden, w.w_kva, w.kva_norm, cfg)
+    kvb = (c_kv @ w.w_kvb).view(-1, H, cfg.qk_nope + cfg.v_head)
+    k_nope = kvb[..., :cfg.qk_nope].reshape(-1, H * cfg.qk_nope)
+    v = kvb[..., cfg.qk_nope:].reshape(-1, H * cfg.v_head)
+    o = _mla_attend(q_nope, _rope(q_pe, cfg.rope_theta), k_nope, _rope(k_pe, cfg.rope_theta), v,
+                    H, cfg, causal)
+    return o @ w.w_o
+
+
+def bd_mla_forward(hidden: torch.Tensor, w: BDMLAWeights, *, causal: bool = True,
+                   group=None) -> torch.Tensor:
+    """BD MLA block: K'_nope and V' of all (local) heads in ONE launch of the BD kernel.
+    With head-sharded weights (``shard_bd_mla``) the partial outputs are summed with one
+    all_reduce over ``group``."""
+    cfg, H = w.cfg, w.n_heads
+    q_nope, q_pe = _split_q(hidden @ w.w_q, H, cfg)
+    c_kv, k_pe = _latent(hidden, w.w_kva, w.kva_norm, cfg)
+    k_nope, v = fused_kv_proj_grouped(c_kv, [(w.c_qk, cfg.qk_nope, H, w.qk_tag),
+                                             (w.c_vo, cfg.v_head, H, w.vo_tag)])
+    o = _mla_attend(q_nope, _rope(q_pe, cfg.rope_theta), k_nope, _rope(k_pe, cfg.rope_theta), v,
+                    H, cfg, causal)
+    out = o @ w.b_vo
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(out, group=group)
+    return out
+
+
+def block_flops(L: int, cfg: MLAConfig, n_heads: int | None = None, bd: bool = True,
+                causal: bool = True) -> int:
+    """Multiply-FLOPs of one block forward over L tokens for n_heads (default all)."""
+    H = cfg.n_heads if n_heads is None else n_heads
+    r = cfg.kv_lora_rank
+    f = 2 * L * cfg.hidden * H * cfg.qk_head                         # q_proj
+    f += 2 * L * cfg.hidden * (r + cfg.qk_rope)                       # kv_a (replicated)
+    f += 2 * L * (r - (cfg.qk_nope if bd else 0)) * H * cfg.qk_nope   # K (nope)
+    f += 2 * L * (r - (cfg.v_head if bd else 0)) * H * cfg.v_head     # V
+    pairs = L * (L + 1) // 2 if causal else L * L
+    f += 2 * pairs * H * (cfg.qk_head + cfg.v_head)                   # QK^T and PV
+    f += 2 * L * H * cfg.v_head * cfg.hidden                          # o_proj
+    return f

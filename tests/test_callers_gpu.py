@@ -85,7 +85,7 @@ def test_bda_forward_causal_and_fp16(cuda):
     got16 = bd.bda_forward(x64.half(), p.to(cuda).cast(torch.float16), causal=True)
     err16 = bd.max_relative_error(got16, ref)
     print("fp16 bda vs fp64 mha max-rel", err16)
-    assert err16 <= 1e-1
+    assert err16 <= 3e-2  # measured 9.0e-3 (B200, round 1)
 
 
 def test_input_validation(cuda):
