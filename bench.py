@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--tokens", type=int, default=CFG2["L"], help="tokens per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-block", action="store_true",
+                    help="skip the DeepSeek-V2-Lite BDA block measurement (config 5)")
+    ap.add_argument("--block-tokens", type=int, default=32768)
     return ap.parse_args()
 
 
@@ -301,17 +304,16 @@ def run_ours(args, rank, world, local):
     # dense cuBLAS comparator first (also settles clocks)
     gdw, _ = capture(dense_step, args.warmup)
     gdt, _ = capture(dense_step, args.steps)
-    dense_ms = timed(gdw, gdt)
+    dense_ms = statistics.median(timed(gdw, gdt) for _ in range(3))
 
     gbw, _ = capture(bd_step, args.warmup)
     gbt, launches = capture(bd_step, args.steps)
     sampler = ClockSampler(local)
     sampler.start()
-    bd_ms = timed(gbw, gbt)
+    runs = [timed(gbw, gbt) for _ in range(3)]
     sampler.stop()
-    # second measurement of the kernel alone for the roofline (same graph)
-    bd_ms2 = timed(gbw, gbt)
-    kern_ms = min(bd_ms, bd_ms2) / args.steps
+    bd_ms = statistics.median(runs)
+    kern_ms = bd_ms / args.steps  # the step is exactly one launch of the kernel
 
     ms_per_step = bd_ms / args.steps
     # L already counts every rank's tokens: each rank projects all L tokens for its heads
@@ -327,6 +329,10 @@ def run_ours(args, rank, world, local):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, bd, torch, dist, dev, world, dtype, L, d, d_h, n, cks[0], cvs[0])
+
+    block = None
+    if not args.no_block:
+        block = run_block(args, torch, dist, dev, rank, world, dtype, stream)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -372,6 +378,8 @@ def run_ours(args, rank, world, local):
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if block is not None:
+        line["block"] = block
     if cpu is not None:
         line["cpu_baseline"] = cpu
     if rank == 0:
@@ -379,6 +387,58 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_block(args, torch, dist, dev, rank, world, dtype, stream):
+    """BASELINE config 5: DeepSeek-V2-Lite MLA attention block (q_proj, kv_a + RMSNorm,
+    BD kv_b_proj as ONE grouped launch, RoPE, causal SDPA, o_proj), random-init weights,
+    `--block-tokens` tokens, heads sharded over the ranks (all_reduce of the output),
+    vs the dense block with the original kv_b_proj weight (cuBLAS).  Strong scaling:
+    the token count is fixed as g grows."""
+    from paper_2510_01718_b200 import mla as M
+    cfg = M.DSV2_LITE
+    w = M.gen_random_mla(1234)
+    p = M.mla_prepare(w)  # offline, CPU (global tags), then shard
+    if world > 1:
+        p = M.shard_bd_mla(p, world, rank)
+    p = p.to(dev, dtype)
+    wd = w.to(dev, dtype)
+    L = args.block_tokens
+    g = torch.Generator(device=dev).manual_seed(99)
+    hid = torch.randn(L, cfg.hidden, device=dev, generator=g).to(dtype)
+    steps, warm = 10, 3
+
+    def time_fn(fn):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(steps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    bd_ms = time_fn(lambda: M.bd_mla_forward(hid, p))
+    dense_ms = time_fn(lambda: M.mla_forward(hid, wd)) if world == 1 else None
+    out = {"workload": "cfg5: DeepSeek-V2-Lite MLA block (hidden 2048, 16 heads, kv_lora 512, "
+                       "nope/rope/v 128/64/128), causal, random-init, BD kv_b_proj",
+           "tokens": L, "heads_per_gpu": cfg.n_heads // world, "scaling": "strong",
+           "bd_ms": bd_ms, "bd_tokens_per_s": L / (bd_ms * 1e-3),
+           "bd_flops_per_gpu": M.block_flops(L, cfg, cfg.n_heads // world, bd=True),
+           "qk_tag": p.qk_tag.value, "vo_tag": p.vo_tag.value}
+    if dense_ms is not None:
+        out.update({"dense_ms": dense_ms, "dense_tokens_per_s": L / (dense_ms * 1e-3),
+                    "speedup_vs_dense": dense_ms / bd_ms})
+    return out
 
 
 def run_e2e(args, bd, torch, dist, dev, world, dtype, L, d, d_h, n, ck, cv):

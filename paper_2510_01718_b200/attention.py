@@ -167,11 +167,11 @@ def _attend(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, n_heads: int, d_h
             e = torch.exp(s - s.amax(dim=1, keepdim=True))
             outs.append(_exact_matmul(e / e.sum(dim=1, keepdim=True), v[:, lo:hi].contiguous()))
         return torch.cat(outs, dim=1)
-    qh = q.view(L, n_heads, -1).transpose(0, 1)
-    kh = k.view(L, n_heads, -1).transpose(0, 1)
-    vh = v.view(L, n_heads, -1).transpose(0, 1)
+    qh = q.view(L, n_heads, -1).transpose(0, 1)[None]  # [1, H, L, d_h]: fused SDPA kernels
+    kh = k.view(L, n_heads, -1).transpose(0, 1)[None]
+    vh = v.view(L, n_heads, -1).transpose(0, 1)[None]
     o = F.scaled_dot_product_attention(qh, kh, vh, is_causal=causal, scale=1.0 / math.sqrt(d_h))
-    return o.transpose(0, 1).reshape(L, n_heads * vh.shape[-1])
+    return o[0].transpose(0, 1).reshape(L, n_heads * vh.shape[-1])
 
 
 def _proj(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:

@@ -36,11 +36,18 @@ import numpy as np
 import torch
 import torch.distributed as dist
 import torch.nn.functional as F
+from torch.nn.attention import SDPBackend, sdpa_kernel
 
 from .attention import select_tag
 from .decompose import Axis, Tag, bd_decompose_both, ordered_matmul
 from .errors import ShapeError
 from .kv_proj import fused_kv_proj_grouped
+
+
+# attention-core backends, in preference order (cuDNN first: it supports the MLA head
+# dims 192/128 natively; math covers float64 test shapes)
+_BACKENDS = [SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION,
+             SDPBackend.EFFICIENT_ATTENTION, SDPBackend.MATH]
 
 
 @dataclass(frozen=True)
@@ -199,11 +206,13 @@ def _mla_attend(q_nope, q_pe, k_nope, k_pe, v, n_heads, cfg: MLAConfig, causal=T
     k = torch.cat([k_nope.view(L, n_heads, cfg.qk_nope),
                    k_pe.view(L, 1, cfg.qk_rope).expand(L, n_heads, cfg.qk_rope)], -1)
     vh = v.view(L, n_heads, cfg.v_head)
-    if cfg.v_head != cfg.qk_head:  # fused SDPA kernels want equal head dims: zero-pad V
-        vh = F.pad(vh, (0, cfg.qk_head - cfg.v_head))
-    o = F.scaled_dot_product_attention(q.transpose(0, 1), k.transpose(0, 1), vh.transpose(0, 1),
-                                       is_causal=causal, scale=1.0 / math.sqrt(cfg.qk_head))
-    return o.transpose(0, 1)[..., :cfg.v_head].reshape(L, n_heads * cfg.v_head)
+    # [1, H, L, D] views; cuDNN's fused attention takes E=192 with Ev=128 directly
+    # (3.6 ms at 32k tokens on B200, vs 18.7 ms for flash with V zero-padded to 192)
+    with sdpa_kernel(_BACKENDS):
+        o = F.scaled_dot_product_attention(q.transpose(0, 1)[None], k.transpose(0, 1)[None],
+                                           vh.transpose(0, 1)[None], is_causal=causal,
+                                           scale=1.0 / math.sqrt(cfg.qk_head))
+    return o[0].transpose(0, 1).reshape(L, n_heads * cfg.v_head)
 
 
 def _split_q(q: torch.Tensor, n_heads: int, cfg: MLAConfig):
