@@ -122,14 +122,40 @@ __device__ __forceinline__ float2 unpack2(uint32_t w) {
   }
 }
 
-// max that propagates NaN (PTX max.NaN), so one running value flags NaN and overflow.
-__device__ __forceinline__ float fmax_nan(float a, float b) {
-  float r;
-  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
-  return r;
+// Packed FP32 add (FADD2 on sm_100): two lanes per instruction, each rounded once.
+__device__ __forceinline__ float2 add_f32x2(float2 a, float2 b) {
+  unsigned long long av = *reinterpret_cast<unsigned long long*>(&a);
+  unsigned long long bv = *reinterpret_cast<unsigned long long*>(&b);
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(av), "l"(bv));
+  return *reinterpret_cast<float2*>(&r);
 }
 
-template <bool kBF16, int CG>
+// Running packed max of |h| that propagates NaN (one HMNMX2 per two outputs).
+template <bool kBF16>
+__device__ __forceinline__ uint32_t max_abs2_nan(uint32_t acc, uint32_t w) {
+  if constexpr (kBF16) {
+    __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&acc);
+    __nv_bfloat162 b = __habs2(*reinterpret_cast<__nv_bfloat162*>(&w));
+    __nv_bfloat162 m = __hmax2_nan(a, b);
+    return *reinterpret_cast<uint32_t*>(&m);
+  } else {
+    __half2 a = *reinterpret_cast<__half2*>(&acc);
+    __half2 b = __habs2(*reinterpret_cast<__half2*>(&w));
+    __half2 m = __hmax2_nan(a, b);
+    return *reinterpret_cast<uint32_t*>(&m);
+  }
+}
+
+// Either 16-bit lane of a packed max is Inf or NaN (exponent bits all ones).
+template <bool kBF16>
+__device__ __forceinline__ bool nonfinite2(uint32_t w) {
+  const uint32_t e = kBF16 ? 0x7F80u : 0x7C00u;
+  return ((w & e) == e) || (((w >> 16) & e) == e);
+}
+
+// kCheck: compute the non-finite flag (only instantiated work when the caller asked).
+template <bool kBF16, int CG, bool kCheck>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     kv_proj_tc_kernel(const __grid_constant__ TcParams prm) {
   using C = Cfg<CG>;
@@ -246,7 +272,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader)
-    if (lane == 0 && rank == 0) {
+    // The whole warp runs the loop (warp-uniform control flow keeps the descriptors in
+    // uniform registers); one elected lane issues the tcgen05 instructions.
+    if (rank == 0) {
       constexpr uint32_t idesc =
           make_idesc_f16(kBF16, BM * CG, BN, /*a_mn=*/false, /*b_mn=*/true);
       int stage = 0;
@@ -266,26 +294,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+          if (elect_one()) {
 #pragma unroll
-          for (int ks = 0; ks < BK / UK; ++ks) {
-            // A: K-major SW128, rows 128 B apart, 8-row groups 1024 B apart; a 16-wide
-            //    k step is +32 B inside the swizzle row.
-            const uint64_t adesc = make_smem_desc(a0 + ks * (UK * 2), 16, 1024);
-            // B: MN-major SW128, 64-column panels B_PANEL apart (LBO), 8-k-row groups
-            //    1024 B apart (SBO); a 16-deep k step is two 8-row groups = 2048 B.
-            const uint64_t bdesc = make_smem_desc(b0 + ks * (UK * 128), B_PANEL, 1024);
-            if constexpr (CG == 1)
-              tc_mma_f16(d_tmem, adesc, bdesc, idesc, (kb | ks) != 0 ? 1u : 0u);
-            else
-              tc_mma_f16_pair(d_tmem, adesc, bdesc, idesc, (kb | ks) != 0 ? 1u : 0u);
+            for (int ks = 0; ks < BK / UK; ++ks) {
+              // A: K-major SW128, rows 128 B apart, 8-row groups 1024 B apart; a 16-wide
+              //    k step is +32 B inside the swizzle row.
+              const uint64_t adesc = make_smem_desc(a0 + ks * (UK * 2), 16, 1024);
+              // B: MN-major SW128, 64-column panels B_PANEL apart (LBO), 8-k-row groups
+              //    1024 B apart (SBO); a 16-deep k step is two 8-row groups = 2048 B.
+              const uint64_t bdesc = make_smem_desc(b0 + ks * (UK * 128), B_PANEL, 1024);
+              if constexpr (CG == 1)
+                tc_mma_f16(d_tmem, adesc, bdesc, idesc, (kb | ks) != 0 ? 1u : 0u);
+              else
+                tc_mma_f16_pair(d_tmem, adesc, bdesc, idesc, (kb | ks) != 0 ? 1u : 0u);
+            }
+            if constexpr (CG == 1) tc_commit(&empty[stage]); else tc_commit_pair(&empty[stage], 0x3);
           }
-          if constexpr (CG == 1) tc_commit(&empty[stage]); else tc_commit_pair(&empty[stage], 0x3);
+          __syncwarp();
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if constexpr (CG == 1) tc_commit(&tfull[acc]); else tc_commit_pair(&tfull[acc], 0x3);
+        if (elect_one()) {
+          if constexpr (CG == 1) tc_commit(&tfull[acc]); else tc_commit_pair(&tfull[acc], 0x3);
+        }
+        __syncwarp();
       }
     }
   } else {
@@ -304,7 +338,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tempty_leader0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
     const uint32_t tempty_leader1 = CG == 2 ? mapa_shared(smem_u32(&tempty[1]), 0) : 0u;
     uint32_t sbuf = 0;
-    float amax = 0.f;  // NaN-propagating max |out| for the non-finite check
+    uint32_t chk = 0u;  // NaN-propagating packed max |out| (16-bit) for the non-finite check
     int rslot = 1;
     uint32_t rphase = 0;  // bit s = parity of rep slot s
     int prev_key = -1;
@@ -371,12 +405,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint32_t o[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
+            // + rep in FP32 (one packed FADD2 per pair), one rounding to 16 bit
             const float2 xr = unpack2<kBF16>(xw[e]);
-            const float v0 = __fadd_rn(__uint_as_float(r[8 * g + 2 * e]), xr.x);
-            const float v1 = __fadd_rn(__uint_as_float(r[8 * g + 2 * e + 1]), xr.y);
-            amax = fmax_nan(amax, fabsf(v0));
-            amax = fmax_nan(amax, fabsf(v1));
-            o[e] = pack2<kBF16>(v0, v1);
+            const float2 v = add_f32x2(make_float2(__uint_as_float(r[8 * g + 2 * e]),
+                                                   __uint_as_float(r[8 * g + 2 * e + 1])), xr);
+            o[e] = pack2<kBF16>(v.x, v.y);
+            if constexpr (kCheck) chk = max_abs2_nan<kBF16>(chk, o[e]);
           }
           const uint32_t dst = stg + row_w * 64 + ((static_cast<uint32_t>(g) ^ sw64) << 4);
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(o[0]),
@@ -412,7 +446,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (!(prm.debug & 2)) process(rb, sub + 1);
           }
         }
-        if (prm.debug & 2) amax = fmax_nan(amax, __uint_as_float(ra[0] & 1u));
+        if (prm.debug & 2) chk |= ra[0] & 1u;
       }
       tc_fence_before();
       named_bar_sync(1, 32 * EPI_WARPS);  // all epilogue threads finished with TMEM + rep
@@ -428,10 +462,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
     if (lane == 0) tma_store_wait_all<0>();
-    // values at or beyond the rounding threshold become Inf in the 16-bit output
-    const float limit = kBF16 ? __uint_as_float(0x7F7F8000u) : 65520.f;
-    const bool bad = !(amax < limit);
-    if (prm.flag != nullptr && __any_sync(0xffffffffu, bad) && lane == 0) atomicExch(prm.flag, 1);
+    // the rounded 16-bit outputs: any Inf/NaN (overflowing sums round to Inf) raises the flag
+    if constexpr (kCheck) {
+      const bool bad = nonfinite2<kBF16>(chk);
+      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(prm.flag, 1);
+    }
   }
 
   tc_fence_before();
@@ -491,11 +526,7 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
     const char* e = getenv("BD_TC_DEBUG");
     return e ? atoi(e) : 0;
   }();
-  // cta_group: 2 (CTA pairs) by default; BD_TC_CTA_GROUP=1 selects the single-CTA kernel.
-  static const int cg = [] {
-    const char* e = getenv("BD_TC_CTA_GROUP");
-    return (e && atoi(e) == 1) ? 1 : 2;
-  }();
+  constexpr int cg = 2;  // CTA pairs (tcgen05 cta_group::2)
   const bool bf16 = dtype == BD_BF16;
   TcParams prm{};
   prm.count = count;
@@ -539,24 +570,19 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
   if (total == 0) return BD_OK;
 
   using KernFn = void (*)(TcParams);
-  KernFn kern;
-  size_t smem;
-  if (cg == 2) {
-    kern = bf16 ? kv_proj_tc_kernel<true, 2> : kv_proj_tc_kernel<false, 2>;
-    smem = Cfg<2>::SMEM_BYTES;
-  } else {
-    kern = bf16 ? kv_proj_tc_kernel<true, 1> : kv_proj_tc_kernel<false, 1>;
-    smem = Cfg<1>::SMEM_BYTES;
-  }
+  const bool check = flag != nullptr;
+  KernFn kern = bf16 ? (check ? kv_proj_tc_kernel<true, 2, true> : kv_proj_tc_kernel<true, 2, false>)
+                     : (check ? kv_proj_tc_kernel<false, 2, true> : kv_proj_tc_kernel<false, 2, false>);
+  const size_t smem = Cfg<2>::SMEM_BYTES;
   static bool attr_set[2][2] = {{false, false}, {false, false}};
-  if (!attr_set[cg - 1][bf16 ? 1 : 0]) {
+  if (!attr_set[bf16 ? 1 : 0][check ? 1 : 0]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) {
       set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
       return BD_ERR_CUDA;
     }
-    attr_set[cg - 1][bf16 ? 1 : 0] = true;
+    attr_set[bf16 ? 1 : 0][check ? 1 : 0] = true;
   }
   const int units = sm_count() / cg;
   const int grid_units = total < units ? total : units;
