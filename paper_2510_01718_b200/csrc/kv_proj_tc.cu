@@ -5,21 +5,32 @@
 // (ref: pkg/src/bdattn/attention.py:249-270 computes the same thing on the CPU.)
 // With rep_base < 0 the same kernel is a plain GEMM (the BD low-rank layer, linear.py).
 //
-// Structure (one persistent CTA per SM, warp-specialised):
-//   warp 0      TMA producer: A = x[:, mul_base : mul_base+K] as a K-major operand
-//               (tensor map based at column mul_base, so the basis slice S is never
-//               read by the mainloop and K tails are zero-filled by TMA), and
-//               B = c in the reference's own (d-d_h) x N row-major layout, loaded as an
-//               MN-major operand (no transpose anywhere).  128B swizzle on both.
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16),
-//               accumulating in FP32 in TMEM; tcgen05.commit releases smem stages and
-//               signals the epilogue.
-//   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns per warp), + x[i, rep_base
-//               + (col mod d_h)] in FP32 (the identity-block gather-add, after the full
-//               K-sum like the reference), one rounding to FP16/BF16, 16-byte stores.
-//               Non-finite outputs raise a device flag (ref _wrap check, tensor.py:112).
-//   TMEM holds two 128x256 FP32 accumulators (all 512 columns) so the epilogue of
-//   tile i overlaps the MMAs of tile i+1.
+// One persistent CTA PAIR (cluster of 2, tcgen05 cta_group::2) per two SMs computes
+// 256 x 256 output tiles; each CTA owns 128 rows (its TMEM lanes) and stages half of
+// the B tile.  Warp roles per CTA:
+//   warp 0      TMA producer.  A = x[:, mul_base : mul_base+K] as a K-major operand
+//               (tensor map based at column mul_base: the basis slice S is never read by
+//               the mainloop; K tails zero-filled by TMA).  B = c in the reference's own
+//               (d-d_h) x N row-major layout as an MN-major operand (no transpose).
+//   warp 1      TMEM allocator + (pair leader) the MMA issuer: the whole warp runs the
+//               loop, one elected lane issues tcgen05.mma (M=256, N=256, K=16, FP32
+//               accumulate in TMEM) and tcgen05.commit.
+//   warps 2..9  epilogue: tcgen05.ld, + x[i, rep_base + (col mod d_h)] in FP32 (the
+//               identity-block gather-add, after the full K-sum like the reference),
+//               one rounding, swizzled smem staging, TMA store.  Optional non-finite
+//               flag (the reference's _wrap check, tensor.py:112-113).
+//
+// A is RESIDENT per row-block: with K = d - d_h <= 384 (DeepSeek-V2-Lite kv_b_proj, the
+// paper's d = 512 shapes) the CTA's whole A row-block (128 x K, <= 96 KiB) sits in six
+// 16 KiB slots and is reused by every n-tile of that row-block, so per tile only B
+// streams and the pair's TMA traffic halves.  Larger K streams through the six slots
+// as a ring.  Slots are released per k-block by tcgen05.commit after their last MMA, so
+// the next row-block's A streams in while the previous tile's MMAs drain.
+//
+// TMEM holds two 128 x 256 FP32 accumulators (all 512 columns): the epilogue of tile i
+// overlaps the MMAs of tile i+1.  The repeated slice x[m0:m0+128, rep_base:+d_h] is
+// staged once per row-block into one smem slot by the epilogue's own leader thread, so
+// the producer never waits on the epilogue.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -38,33 +49,30 @@
 namespace bdk {
 namespace tc {
 
-constexpr int BM = 128;                       // rows of x per CTA per tile (TMEM lanes)
-constexpr int BN = 256;                       // UMMA N (output columns per tile)
+constexpr int CG = 2;                         // cta_group::2 (CTA pairs)
+constexpr int BM = 128;                       // rows per CTA per tile (TMEM lanes)
+constexpr int BN = 256;                       // UMMA N (output columns per pair tile)
 constexpr int BK = 64;                        // k-block: one 128-byte swizzle row of A
 constexpr int UK = 16;                        // UMMA K for kind::f16
-constexpr int EPI_WARPS = 8;                  // 2 per SMSP; warps w, w+4 share a TMEM lane quadrant
+constexpr int EPI_WARPS = 8;                  // 2 per SMSP; warps w, w+4 share a lane quadrant
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
-constexpr uint32_t A_BYTES = BM * BK * 2;     // 16 KiB
+#ifndef BD_A_SLOTS
+#define BD_A_SLOTS 6
+#endif
+constexpr int A_SLOTS = BD_A_SLOTS;           // resident A: K <= 6 * 64 = 384
+constexpr int B_STAGES = 4;
+constexpr uint32_t A_BYTES = BM * BK * 2;     // 16 KiB: 128 rows x 64 k
 constexpr uint32_t B_PANEL = 64 * BK * 2;     // one 64-column MN-major swizzle panel, 8 KiB
+constexpr int B_PANELS = (BN / 64) / CG;      // this CTA's half of the B tile: 2 panels
+constexpr uint32_t B_BYTES = B_PANELS * B_PANEL;
 constexpr uint32_t REP_BOX = 64 * BM * 2;     // one 64-column x 128-row rep box, 16 KiB
 constexpr uint32_t REP_BYTES = 2 * REP_BOX;   // d_h <= 128 -> at most two boxes
 constexpr uint32_t STG_BYTES = 32 * 32 * 2;   // output staging box: 32 rows x 32 cols (SW64)
+constexpr int STG_BUFS = 2;                   // per-warp staging buffers
 constexpr uint32_t TMEM_COLS = 2 * BN;        // double-buffered accumulator
-
-// Per cta_group configuration.  CG = 2: a CTA pair computes a 256 x 256 tile with
-// tcgen05.mma.cta_group::2 — each CTA stages its own 128 rows of A and HALF of the B
-// tile (128 columns), so B bytes per CTA halve and the ring can be one stage deeper.
-template <int CG>
-struct Cfg {
-  static constexpr int B_PANELS = (BN / 64) / CG;               // 4 (CG=1) / 2 (CG=2)
-  static constexpr uint32_t B_BYTES = B_PANELS * B_PANEL;
-  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;    // 48 / 32 KiB
-  static constexpr int STAGES = CG == 1 ? 3 : 4;
-  static constexpr int STG_BUFS = CG == 1 ? 1 : 2;               // per-warp staging buffers
-  static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 2 * REP_BYTES +
-                                       EPI_WARPS * STG_BUFS * STG_BYTES + 256;
-  static_assert(SMEM_BYTES <= 232448, "shared memory budget");
-};
+constexpr size_t SMEM_BYTES = 1024 + A_SLOTS * A_BYTES + B_STAGES * B_BYTES + REP_BYTES +
+                              EPI_WARPS * STG_BUFS * STG_BYTES + 256;
+static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
 struct TcProblem {
   CUtensorMap map_a;    // x + mul_base, dims {K, L},   box {64, 128}
@@ -83,11 +91,9 @@ struct TcParams {
   TcProblem p[BD_MAX_GROUP];
   int32_t count;
   int32_t total_tiles;  // tiles of (BM * CG) rows x BN columns
-  int* flag;
-  int32_t debug;  // profiling knob (env BD_TC_DEBUG): 1 no stores, 2 no epilogue math, 4 no LDTM
+  int* flag;            // non-finite flag (kCheck instantiation only)
 };
 
-template <int CG>
 __device__ __forceinline__ void decode_tile(const TcParams& prm, int t, int& pi, int& m0,
                                             int& n0) {
   pi = 0;
@@ -97,8 +103,8 @@ __device__ __forceinline__ void decode_tile(const TcParams& prm, int t, int& pi,
   m0 = (local / prm.p[pi].tiles_n) * (BM * CG);
 }
 
-// Tiles sharing (problem, m-block) share the rep tile x[m0:m0+128, rep_base:+d_h].
-__device__ __forceinline__ int rep_key(int pi, int m0) { return (pi << 24) | (m0 / BM); }
+// Tiles sharing (problem, pair row-block) share the A row-block and the rep tile.
+__device__ __forceinline__ int blk_key(int pi, int m0) { return (pi << 24) | (m0 / (BM * CG)); }
 
 template <bool kBF16>
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -154,33 +160,33 @@ __device__ __forceinline__ bool nonfinite2(uint32_t w) {
   return ((w & e) == e) || (((w >> 16) & e) == e);
 }
 
-// kCheck: compute the non-finite flag (only instantiated work when the caller asked).
-template <bool kBF16, int CG, bool kCheck>
+// kCheck: compute the non-finite flag (instantiated only when the caller asked for it).
+template <bool kBF16, bool kCheck>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     kv_proj_tc_kernel(const __grid_constant__ TcParams prm) {
-  using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = sA + C::STAGES * A_BYTES;
-  uint8_t* sRep = sB + C::STAGES * C::B_BYTES;      // 2 slots x REP_BYTES
-  uint8_t* sStg = sRep + 2 * REP_BYTES;             // EPI_WARPS x STG_BUFS x STG_BYTES
-  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + EPI_WARPS * C::STG_BUFS * STG_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;
+  uint8_t* sB = sA + A_SLOTS * A_BYTES;
+  uint8_t* sRep = sB + B_STAGES * B_BYTES;
+  uint8_t* sStg = sRep + REP_BYTES;                 // EPI_WARPS x STG_BUFS x STG_BYTES
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sStg + EPI_WARPS * STG_BUFS * STG_BYTES);
+  uint64_t* a_empty = a_full + A_SLOTS;
+  uint64_t* b_full = a_empty + A_SLOTS;
+  uint64_t* b_empty = b_full + B_STAGES;
+  uint64_t* tfull = b_empty + B_STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* rfull = tempty + 2;
-  uint64_t* rempty = rfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 1);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;  // 0 = pair leader
-  const int unit = CG == 2 ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
-  const int units = CG == 2 ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
-  // Contiguous tile range per CTA (pair): consecutive tiles share the x row-block (A and
-  // the rep slice stay L2/smem-hot); the split is balanced to within one tile.
+  const uint32_t rank = cluster_ctarank();  // 0 = pair leader
+  const int unit = static_cast<int>(blockIdx.x >> 1);
+  const int units = static_cast<int>(gridDim.x >> 1);
+  // Contiguous tile range per pair: consecutive tiles share the row-block (A resident,
+  // rep tile reused); the split is balanced to within one tile.
   const int t_begin = static_cast<int>(static_cast<int64_t>(unit) * prm.total_tiles / units);
   const int t_end = static_cast<int>(static_cast<int64_t>(unit + 1) * prm.total_tiles / units);
 
@@ -191,16 +197,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tma_prefetch_desc(&prm.p[i].map_out);
       if (prm.p[i].rep_fast) tma_prefetch_desc(&prm.p[i].map_rep);
     }
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], 1);    // armed by the leader's producer with the pair's bytes
-      mbar_init(&empty[s], 1);   // one (multicast) tcgen05.commit
+    for (int s = 0; s < A_SLOTS; ++s) {
+      mbar_init(&a_full[s], 1);   // armed by the leader's producer with the pair's bytes
+      mbar_init(&a_empty[s], 1);  // one multicast tcgen05.commit
+    }
+    for (int s = 0; s < B_STAGES; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], CG);  // one arrival per CTA's epilogue (leader's copy)
-      mbar_init(&rfull[a], 1);
-      mbar_init(&rempty[a], 1);
     }
+    mbar_init(rfull, 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -208,7 +217,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tmem_relinquish<CG>();
   }
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -216,57 +225,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_last();  // x and c are re-read; out streams past
-      int stage = 0;
-      uint32_t phase = 0;
-      int rslot = 1;
-      uint32_t rphase = 0;  // bit s = parity of rep slot s
+      uint32_t a_iter = 0, b_iter = 0;
       int prev_key = -1;
       for (int t = t_begin; t < t_end; ++t) {
         int pi, m0, n0;
-        decode_tile<CG>(prm, t, pi, m0, n0);
+        decode_tile(prm, t, pi, m0, n0);
         const TcProblem& P = prm.p[pi];
+        const int key = blk_key(pi, m0);
+        const bool reload_a = P.num_kb > A_SLOTS || key != prev_key;
+        prev_key = key;
         const int my_m0 = m0 + static_cast<int>(rank) * BM;
         const int my_n0 = n0 + static_cast<int>(rank) * (BN / CG);
-        const int key = rep_key(pi, my_m0);
-        if (P.rep_fast && key != prev_key) {
-          // New (problem, m-block): stage its rep tile in the other slot.
-          rslot ^= 1;
-          mbar_wait(&rempty[rslot], ((rphase >> rslot) & 1u) ^ 1u);
-          rphase ^= 1u << rslot;
-          const int nbox = P.d_h / 64;
-          mbar_arrive_expect_tx(&rfull[rslot], nbox * REP_BOX);
-          for (int b = 0; b < nbox; ++b)
-            tma_load_2d(sRep + rslot * REP_BYTES + b * REP_BOX, &P.map_rep, 64 * b, my_m0,
-                        &rfull[rslot], pol);
-        }
-        prev_key = key;
         for (int kb = 0; kb < P.num_kb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* a_dst = sA + stage * A_BYTES;
-          uint8_t* b_dst = sB + stage * C::B_BYTES;
-          if constexpr (CG == 1) {
-            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-            tma_load_2d(a_dst, &P.map_a, kb * BK, my_m0, &full[stage], pol);
-#pragma unroll
-            for (int q = 0; q < C::B_PANELS; ++q)
-              tma_load_2d(b_dst + q * B_PANEL, &P.map_b, my_n0 + 64 * q, kb * BK, &full[stage],
-                          pol);
-          } else {
-            // Both CTAs' bytes complete on the LEADER's full barrier, which the leader
-            // arms with the pair's total.  The peer does not arrive: a cluster-scope
-            // release arrive would stall it on its own in-flight TMA loads, and the
-            // barrier cannot complete before the leader's arrival anyway.
-            const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
-            if (rank == 0) mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
-            tma_load_2d_pair(a_dst, &P.map_a, kb * BK, my_m0, bar, pol);
-#pragma unroll
-            for (int q = 0; q < C::B_PANELS; ++q)
-              tma_load_2d_pair(b_dst + q * B_PANEL, &P.map_b, my_n0 + 64 * q, kb * BK, bar, pol);
+          // Both CTAs' bytes complete on the LEADER's barriers, which the leader arms with
+          // the pair's total.  The peer does not arrive: the barrier cannot complete
+          // before the leader's arrival, and each CTA only refills a slot after the
+          // multicast commit released it, i.e. after the previous phase completed.
+          if (reload_a) {
+            const uint32_t s = a_iter % A_SLOTS;
+            mbar_wait(&a_empty[s], ((a_iter / A_SLOTS) & 1u) ^ 1u);
+            if (rank == 0) mbar_arrive_expect_tx(&a_full[s], CG * A_BYTES);
+            tma_load_2d_pair(sA + s * A_BYTES, &P.map_a, kb * BK, my_m0,
+                             mapa_shared(smem_u32(&a_full[s]), 0), pol);
+            ++a_iter;
           }
-          if (++stage == C::STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+          const uint32_t s = b_iter % B_STAGES;
+          mbar_wait(&b_empty[s], ((b_iter / B_STAGES) & 1u) ^ 1u);
+          if (rank == 0) mbar_arrive_expect_tx(&b_full[s], CG * B_BYTES);
+          const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), 0);
+#pragma unroll
+          for (int q = 0; q < B_PANELS; ++q)
+            tma_load_2d_pair(sB + s * B_BYTES + q * B_PANEL, &P.map_b, my_n0 + 64 * q, kb * BK,
+                             bar, pol);
+          ++b_iter;
         }
       }
     }
@@ -277,23 +268,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (rank == 0) {
       constexpr uint32_t idesc =
           make_idesc_f16(kBF16, BM * CG, BN, /*a_mn=*/false, /*b_mn=*/true);
-      int stage = 0;
-      uint32_t phase = 0;
+      uint32_t a_iter = 0, a_base = 0, b_iter = 0;
+      int prev_key = -1;
       int it = 0;
       for (int t = t_begin; t < t_end; ++t, ++it) {
         int pi, m0, n0;
-        decode_tile<CG>(prm, t, pi, m0, n0);
+        decode_tile(prm, t, pi, m0, n0);
         const TcProblem& P = prm.p[pi];
+        const int key = blk_key(pi, m0);
+        const bool stream_a = P.num_kb > A_SLOTS;
+        const bool reload_a = stream_a || key != prev_key;
+        prev_key = key;
+        // Last tile reading this A row-block: release each slot after its k-block's MMAs.
+        bool last_use = true;
+        if (!stream_a && t + 1 < t_end) {
+          int npi, nm0, nn0;
+          decode_tile(prm, t + 1, npi, nm0, nn0);
+          last_use = blk_key(npi, nm0) != key;
+        }
+        if (reload_a) {
+          a_base = a_iter;
+          a_iter += P.num_kb;
+        }
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < P.num_kb; ++kb) {
-          mbar_wait(&full[stage], phase);
+          const uint32_t ai = a_base + kb;
+          const uint32_t as = ai % A_SLOTS;
+          if (reload_a) mbar_wait(&a_full[as], (ai / A_SLOTS) & 1u);
+          const uint32_t bs = b_iter % B_STAGES;
+          mbar_wait(&b_full[bs], (b_iter / B_STAGES) & 1u);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+          const uint32_t a0 = smem_u32(sA + as * A_BYTES);
+          const uint32_t b0 = smem_u32(sB + bs * B_BYTES);
           if (elect_one()) {
 #pragma unroll
             for (int ks = 0; ks < BK / UK; ++ks) {
@@ -303,22 +313,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               // B: MN-major SW128, 64-column panels B_PANEL apart (LBO), 8-k-row groups
               //    1024 B apart (SBO); a 16-deep k step is two 8-row groups = 2048 B.
               const uint64_t bdesc = make_smem_desc(b0 + ks * (UK * 128), B_PANEL, 1024);
-              if constexpr (CG == 1)
-                tc_mma_f16(d_tmem, adesc, bdesc, idesc, (kb | ks) != 0 ? 1u : 0u);
-              else
-                tc_mma_f16_pair(d_tmem, adesc, bdesc, idesc, (kb | ks) != 0 ? 1u : 0u);
+              tc_mma_f16_pair(d_tmem, adesc, bdesc, idesc, (kb | ks) != 0 ? 1u : 0u);
             }
-            if constexpr (CG == 1) tc_commit(&empty[stage]); else tc_commit_pair(&empty[stage], 0x3);
+            tc_commit_pair(&b_empty[bs], 0x3);
+            if (last_use) tc_commit_pair(&a_empty[as], 0x3);
           }
           __syncwarp();
-          if (++stage == C::STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+          ++b_iter;
         }
-        if (elect_one()) {
-          if constexpr (CG == 1) tc_commit(&tfull[acc]); else tc_commit_pair(&tfull[acc], 0x3);
-        }
+        if (elect_one()) tc_commit_pair(&tfull[acc], 0x3);
         __syncwarp();
       }
     }
@@ -333,30 +336,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int row_w = static_cast<int>(lane);
     const int row_t = static_cast<int>(quad * 32) + row_w;
     const bool leader = (ew == 0 && lane == 0);
-    const uint32_t stg0 = smem_u32(sStg + ew * C::STG_BUFS * STG_BYTES);
+    const uint32_t stg0 = smem_u32(sStg + ew * STG_BUFS * STG_BYTES);
     const uint32_t sw64 = static_cast<uint32_t>((row_w >> 1) & 3);
-    const uint32_t tempty_leader0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
-    const uint32_t tempty_leader1 = CG == 2 ? mapa_shared(smem_u32(&tempty[1]), 0) : 0u;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
+    const uint8_t* rep_row = sRep + row_t * 128;
+    // leader only: stage the rep tile of tile t (this CTA's 128 rows) into the slot
+    auto issue_rep = [&](int t) {
+      int pi, m0, n0;
+      decode_tile(prm, t, pi, m0, n0);
+      const TcProblem& P = prm.p[pi];
+      const int nbox = P.d_h / 64;
+      mbar_arrive_expect_tx(rfull, nbox * REP_BOX);
+      for (int b = 0; b < nbox; ++b)
+        tma_load_2d(sRep + b * REP_BOX, &P.map_rep, 64 * b, m0 + static_cast<int>(rank) * BM,
+                    rfull, policy_evict_last());
+    };
+    if (leader && t_begin < t_end) {
+      int pi, m0, n0;
+      decode_tile(prm, t_begin, pi, m0, n0);
+      if (prm.p[pi].rep_fast) issue_rep(t_begin);
+    }
     uint32_t sbuf = 0;
     uint32_t chk = 0u;  // NaN-propagating packed max |out| (16-bit) for the non-finite check
-    int rslot = 1;
-    uint32_t rphase = 0;  // bit s = parity of rep slot s
-    int prev_key = -1;
+    uint32_t rep_loads = 0;
+    int cur_key = -1;   // row-block whose rep tile is in the slot (-1: none)
     int it = 0;
     for (int t = t_begin; t < t_end; ++t, ++it) {
       int pi, m0, n0;
-      decode_tile<CG>(prm, t, pi, m0, n0);
+      decode_tile(prm, t, pi, m0, n0);
       const TcProblem& P = prm.p[pi];
       const int my_m0 = m0 + static_cast<int>(rank) * BM;
-      const int key = rep_key(pi, my_m0);
+      const int key = blk_key(pi, m0);
       const bool fast = P.rep_fast != 0;
-      if (fast && key != prev_key) {
-        rslot ^= 1;
-        mbar_wait(&rfull[rslot], (rphase >> rslot) & 1u);
-        rphase ^= 1u << rslot;
+      if (fast && key != cur_key) {
+        mbar_wait(rfull, rep_loads & 1u);
+        ++rep_loads;
+        cur_key = key;
       }
-      prev_key = key;
-      const uint8_t* rep_row = sRep + rslot * REP_BYTES + row_t * 128;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -397,7 +414,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         const uint32_t stg = stg0 + sbuf * STG_BYTES;
         // the TMA store that last read this staging buffer must be done with it
-        if (lane == 0) tma_store_wait_read<C::STG_BUFS - 1>();
+        if (lane == 0) tma_store_wait_read<STG_BUFS - 1>();
         __syncwarp();
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
@@ -419,7 +436,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0 && !(prm.debug & 1)) {
+        if (lane == 0) {
           asm volatile(
               "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                   reinterpret_cast<uint64_t>(&P.map_out)),
@@ -427,10 +444,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               : "memory");
           tma_store_commit();
         }
-        if constexpr (C::STG_BUFS > 1) sbuf ^= 1;
+        sbuf ^= 1;
       };
 
-      if (!(prm.debug & 4) && nsub > 0) {
+      if (nsub > 0) {
         uint32_t ra[32], rb[32];
         tmem_ld_32x32b_x32(taddr, ra);
 #pragma unroll
@@ -438,26 +455,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (sub < nsub) {
             tmem_ld_wait();
             if (sub + 1 < nsub) tmem_ld_32x32b_x32(taddr + (sub + 1) * 32, rb);
-            if (!(prm.debug & 2)) process(ra, sub);
+            process(ra, sub);
           }
           if (sub + 1 < nsub) {
             tmem_ld_wait();
             if (sub + 2 < nsub) tmem_ld_32x32b_x32(taddr + (sub + 2) * 32, ra);
-            if (!(prm.debug & 2)) process(rb, sub + 1);
+            process(rb, sub + 1);
           }
         }
-        if (prm.debug & 2) chk |= ra[0] & 1u;
       }
       tc_fence_before();
       named_bar_sync(1, 32 * EPI_WARPS);  // all epilogue threads finished with TMEM + rep
       if (leader) {
-        if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
-        else mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
-        if (fast) {
-          int npi = -1, nm0 = 0, nn0 = 0;
-          if (t + 1 < t_end) decode_tile<CG>(prm, t + 1, npi, nm0, nn0);
-          if (t + 1 >= t_end || rep_key(npi, nm0 + static_cast<int>(rank) * BM) != key)
-            mbar_arrive(&rempty[rslot]);
+        mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
+        // the next tile starts a new row-block: restage the rep slot (nobody reads it now)
+        if (t + 1 < t_end) {
+          int npi, nm0, nn0;
+          decode_tile(prm, t + 1, npi, nm0, nn0);
+          if (prm.p[npi].rep_fast && blk_key(npi, nm0) != cur_key) issue_rep(t + 1);
         }
       }
     }
@@ -470,7 +485,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  cluster_sync();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, TMEM_COLS);
@@ -522,16 +537,11 @@ bool encode_2d(CUtensorMap* map, const void* base, bool bf16, uint64_t cols, uin
 
 int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_t stream) {
   using namespace tc;
-  static const int debug = [] {
-    const char* e = getenv("BD_TC_DEBUG");
-    return e ? atoi(e) : 0;
-  }();
-  constexpr int cg = 2;  // CTA pairs (tcgen05 cta_group::2)
+  constexpr int cg = CG;
   const bool bf16 = dtype == BD_BF16;
   TcParams prm{};
   prm.count = count;
   prm.flag = flag;
-  prm.debug = debug;
   int total = 0;
   for (int i = 0; i < count; ++i) {
     const Problem& q = probs[i];
@@ -571,9 +581,9 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
 
   using KernFn = void (*)(TcParams);
   const bool check = flag != nullptr;
-  KernFn kern = bf16 ? (check ? kv_proj_tc_kernel<true, 2, true> : kv_proj_tc_kernel<true, 2, false>)
-                     : (check ? kv_proj_tc_kernel<false, 2, true> : kv_proj_tc_kernel<false, 2, false>);
-  const size_t smem = Cfg<2>::SMEM_BYTES;
+  KernFn kern = bf16 ? (check ? kv_proj_tc_kernel<true, true> : kv_proj_tc_kernel<true, false>)
+                     : (check ? kv_proj_tc_kernel<false, true> : kv_proj_tc_kernel<false, false>);
+  const size_t smem = SMEM_BYTES;
   static bool attr_set[2][2] = {{false, false}, {false, false}};
   if (!attr_set[bf16 ? 1 : 0][check ? 1 : 0]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
