@@ -67,8 +67,8 @@ constexpr int B_PANELS = (BN / 64) / CG;      // this CTA's half of the B tile: 
 constexpr uint32_t B_BYTES = B_PANELS * B_PANEL;
 constexpr uint32_t REP_BOX = 64 * BM * 2;     // one 64-column x 128-row rep box, 16 KiB
 constexpr uint32_t REP_BYTES = 2 * REP_BOX;   // d_h <= 128 -> at most two boxes
-constexpr uint32_t STG_BYTES = 32 * 32 * 2;   // output staging box: 32 rows x 32 cols (SW64)
-constexpr int STG_BUFS = 2;                   // per-warp staging buffers
+constexpr uint32_t STG_BYTES = 32 * 64 * 2;   // output staging box: 32 rows x 64 cols (SW128)
+constexpr int STG_BUFS = 1;                   // per-warp staging buffers
 constexpr uint32_t TMEM_COLS = 2 * BN;        // double-buffered accumulator
 constexpr size_t SMEM_BYTES = 1024 + A_SLOTS * A_BYTES + B_STAGES * B_BYTES + REP_BYTES +
                               EPI_WARPS * STG_BUFS * STG_BYTES + 256;
@@ -78,7 +78,7 @@ struct TcProblem {
   CUtensorMap map_a;    // x + mul_base, dims {K, L},   box {64, 128}
   CUtensorMap map_b;    // c,            dims {N, K},   box {64, 64}
   CUtensorMap map_rep;  // x + rep_base, dims {d_h, L}, box {64, 128}   (rep_fast only)
-  CUtensorMap map_out;  // out,          dims {N, L},   box {32, 32}, SW64
+  CUtensorMap map_out;  // out,          dims {N, L},   box {64, 32}, SW128
   const void* x;
   int64_t ldx;
   int32_t L, N, K, d_h, rep_base;
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int row_t = static_cast<int>(quad * 32) + row_w;
     const bool leader = (ew == 0 && lane == 0);
     const uint32_t stg0 = smem_u32(sStg + ew * STG_BUFS * STG_BYTES);
-    const uint32_t sw64 = static_cast<uint32_t>((row_w >> 1) & 3);
+    const uint32_t sw128 = static_cast<uint32_t>(row_w & 7);
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
     const uint8_t* rep_row = sRep + row_t * 128;
@@ -357,7 +357,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       decode_tile(prm, t_begin, pi, m0, n0);
       if (prm.p[pi].rep_fast) issue_rep(t_begin);
     }
-    uint32_t sbuf = 0;
     uint32_t chk = 0u;  // NaN-propagating packed max |out| (16-bit) for the non-finite check
     uint32_t rep_loads = 0;
     int cur_key = -1;   // row-block whose rep tile is in the slot (-1: none)
@@ -412,10 +411,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         : make_uint4(0, 0, 0, 0);
           }
         }
-        const uint32_t stg = stg0 + sbuf * STG_BYTES;
-        // the TMA store that last read this staging buffer must be done with it
-        if (lane == 0) tma_store_wait_read<STG_BUFS - 1>();
-        __syncwarp();
+        // Two 32-column sub-chunks fill one 32 x 64 staging box; the box's TMA store is
+        // issued after the second.  Before the first writes, the previous box's store must
+        // have finished reading the buffer (it was issued a whole sub-chunk pair ago).
+        const uint32_t stg = stg0;
+        const uint32_t gpart = static_cast<uint32_t>(sub & 1) * 4;
+        if ((sub & 1) == 0) {
+          if (lane == 0) tma_store_wait_read<0>();
+          __syncwarp();
+        }
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const uint32_t xw[4] = {xv[g].x, xv[g].y, xv[g].z, xv[g].w};
@@ -429,22 +433,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             o[e] = pack2<kBF16>(v.x, v.y);
             if constexpr (kCheck) chk = max_abs2_nan<kBF16>(chk, o[e]);
           }
-          const uint32_t dst = stg + row_w * 64 + ((static_cast<uint32_t>(g) ^ sw64) << 4);
+          const uint32_t dst = stg + row_w * 128 + (((gpart + g) ^ sw128) << 4);
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(o[0]),
                        "r"(o[1]), "r"(o[2]), "r"(o[3])
                        : "memory");
         }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          asm volatile(
-              "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                  reinterpret_cast<uint64_t>(&P.map_out)),
-              "r"(stg), "r"(col0), "r"(my_m0 + static_cast<int>(quad) * 32)
-              : "memory");
-          tma_store_commit();
+        if ((sub & 1) == 1 || sub + 1 == nsub) {
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(&P.map_out)),
+                "r"(stg), "r"(col0 - (sub & 1) * 32), "r"(my_m0 + static_cast<int>(quad) * 32)
+                : "memory");
+            tma_store_commit();
+          }
         }
-        sbuf ^= 1;
       };
 
       if (nsub > 0) {
@@ -557,7 +562,7 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
     const auto* xr = static_cast<const uint16_t*>(q.x) + rep_base;
     if (!encode_2d(&P.map_a, xb, bf16, K, q.L, q.ldx, BK, BM, &err) ||
         !encode_2d(&P.map_b, q.c, bf16, N, K, q.ldc, 64, BK, &err) ||
-        !encode_2d(&P.map_out, q.out, bf16, N, q.L, q.ldo, 32, 32, &err, CU_TENSOR_MAP_SWIZZLE_64B) ||
+        !encode_2d(&P.map_out, q.out, bf16, N, q.L, q.ldo, 64, 32, &err) ||
         (rep_fast && !encode_2d(&P.map_rep, xr, bf16, d_h, q.L, q.ldx, 64, BM, &err))) {
       set_error(err);
       return BD_ERR_CUDA;
