@@ -51,7 +51,13 @@ namespace tc {
 
 constexpr int CG = 2;                         // cta_group::2 (CTA pairs)
 constexpr int BM = 128;                       // rows per CTA per tile (TMEM lanes)
-constexpr int BN = 256;                       // UMMA N (output columns per pair tile)
+#ifndef BD_BN
+#define BD_BN 256
+#endif
+constexpr int BN = BD_BN;                     // UMMA N (output columns per pair tile)
+constexpr int NUM_ACC = 512 / BN;             // accumulator buffers in TMEM's 512 columns
+constexpr int WC = BN / 2;                    // accumulator columns per epilogue warp
+constexpr int WSUB = WC / 32;                 // 32-column sub-chunks per warp per tile
 constexpr int BK = 64;                        // k-block: one 128-byte swizzle row of A
 constexpr int UK = 16;                        // UMMA K for kind::f16
 constexpr int EPI_WARPS = 8;                  // 2 per SMSP; warps w, w+4 share a lane quadrant
@@ -69,7 +75,7 @@ constexpr uint32_t REP_BOX = 64 * BM * 2;     // one 64-column x 128-row rep box
 constexpr uint32_t REP_BYTES = 2 * REP_BOX;   // d_h <= 128 -> at most two boxes
 constexpr uint32_t STG_BYTES = 32 * 64 * 2;   // output staging box: 32 rows x 64 cols (SW128)
 constexpr int STG_BUFS = 1;                   // per-warp staging buffers
-constexpr uint32_t TMEM_COLS = 2 * BN;        // double-buffered accumulator
+constexpr uint32_t TMEM_COLS = 512;          // NUM_ACC accumulator buffers
 constexpr size_t SMEM_BYTES = 1024 + A_SLOTS * A_BYTES + B_STAGES * B_BYTES + REP_BYTES +
                               EPI_WARPS * STG_BUFS * STG_BYTES + 256;
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
@@ -128,6 +134,22 @@ __device__ __forceinline__ float2 unpack2(uint32_t w) {
   }
 }
 
+// (a + lo(h), b + hi(h)) in FP32 with the 16-bit halves of h widened exactly: the
+// mixed-precision add.f32.f16 / add.f32.bf16 (one FHADD per element on sm_100).
+template <bool kBF16>
+__device__ __forceinline__ float2 add_f32_x16x2(float a, float b, uint32_t h) {
+  float r0, r1;
+  if constexpr (kBF16)
+    asm("{ .reg .b16 lo, hi; mov.b32 {lo, hi}, %2; add.rn.f32.bf16 %0, lo, %3;"
+        " add.rn.f32.bf16 %1, hi, %4; }"
+        : "=f"(r0), "=f"(r1) : "r"(h), "f"(a), "f"(b));
+  else
+    asm("{ .reg .b16 lo, hi; mov.b32 {lo, hi}, %2; add.rn.f32.f16 %0, lo, %3;"
+        " add.rn.f32.f16 %1, hi, %4; }"
+        : "=f"(r0), "=f"(r1) : "r"(h), "f"(a), "f"(b));
+  return make_float2(r0, r1);
+}
+
 // Packed FP32 add (FADD2 on sm_100): two lanes per instruction, each rounded once.
 __device__ __forceinline__ float2 add_f32x2(float2 a, float2 b) {
   unsigned long long av = *reinterpret_cast<unsigned long long*>(&a);
@@ -176,8 +198,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* b_full = a_empty + A_SLOTS;
   uint64_t* b_empty = b_full + B_STAGES;
   uint64_t* tfull = b_empty + B_STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* rfull = tempty + 2;
+  uint64_t* tempty = tfull + NUM_ACC;
+  uint64_t* rfull = tempty + NUM_ACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 1);
 
   const uint32_t warp = warp_id();
@@ -205,7 +227,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&b_full[s], 1);
       mbar_init(&b_empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NUM_ACC; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], CG);  // one arrival per CTA's epilogue (leader's copy)
     }
@@ -290,8 +312,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           a_base = a_iter;
           a_iter += P.num_kb;
         }
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
+        const int acc = it % NUM_ACC;
+        const uint32_t acc_phase = (it / NUM_ACC) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -338,8 +360,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool leader = (ew == 0 && lane == 0);
     const uint32_t stg0 = smem_u32(sStg + ew * STG_BUFS * STG_BYTES);
     const uint32_t sw128 = static_cast<uint32_t>(row_w & 7);
-    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
-    const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
     const uint8_t* rep_row = sRep + row_t * 128;
     // leader only: stage the rep tile of tile t (this CTA's 128 rows) into the slot
     auto issue_rep = [&](int t) {
@@ -373,18 +393,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ++rep_loads;
         cur_key = key;
       }
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = it % NUM_ACC;
+      const uint32_t acc_phase = (it / NUM_ACC) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t grow = static_cast<int64_t>(my_m0) + row_t;
       const bool has_rep = P.has_rep != 0;
       const uint16_t* xrow = static_cast<const uint16_t*>(P.x) +
                              (grow < P.L ? grow : 0) * P.ldx + P.rep_base;
-      const int cbase = n0 + static_cast<int>(half) * 128;
+      const int cbase = n0 + static_cast<int>(half) * WC;
       int nsub = (P.N - cbase + 31) / 32;
-      nsub = nsub < 0 ? 0 : (nsub > 4 ? 4 : nsub);
-      const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * BN + half * 128;
+      nsub = nsub < 0 ? 0 : (nsub > WSUB ? WSUB : nsub);
+      const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * BN + half * WC;
       const int dmask = P.d_h - 1;
 
       auto process = [&](const uint32_t (&r)[32], int sub) {
@@ -426,10 +446,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint32_t o[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            // + rep in FP32 (one packed FADD2 per pair), one rounding to 16 bit
-            const float2 xr = unpack2<kBF16>(xw[e]);
-            const float2 v = add_f32x2(make_float2(__uint_as_float(r[8 * g + 2 * e]),
-                                                   __uint_as_float(r[8 * g + 2 * e + 1])), xr);
+            // + rep in FP32 with one mixed-precision FHADD per element (exact widening of
+            // the 16-bit rep, one FP32 rounding), then one rounding to 16 bit
+            const float2 v = add_f32_x16x2<kBF16>(__uint_as_float(r[8 * g + 2 * e]),
+                                                 __uint_as_float(r[8 * g + 2 * e + 1]), xw[e]);
             o[e] = pack2<kBF16>(v.x, v.y);
             if constexpr (kCheck) chk = max_abs2_nan<kBF16>(chk, o[e]);
           }
@@ -456,7 +476,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t ra[32], rb[32];
         tmem_ld_32x32b_x32(taddr, ra);
 #pragma unroll
-        for (int sub = 0; sub < 4; sub += 2) {
+        for (int sub = 0; sub < WSUB; sub += 2) {
           if (sub < nsub) {
             tmem_ld_wait();
             if (sub + 1 < nsub) tmem_ld_32x32b_x32(taddr + (sub + 1) * 32, rb);
@@ -472,7 +492,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_before();
       named_bar_sync(1, 32 * EPI_WARPS);  // all epilogue threads finished with TMEM + rep
       if (leader) {
-        mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
+        mbar_arrive_remote(mapa_shared(smem_u32(&tempty[acc]), 0));
         // the next tile starts a new row-block: restage the rep slot (nobody reads it now)
         if (t + 1 < t_end) {
           int npi, nm0, nn0;
