@@ -57,7 +57,6 @@ constexpr int BM = 128;                       // rows per CTA per tile (TMEM lan
 constexpr int BN = BD_BN;                     // UMMA N (output columns per pair tile)
 constexpr int NUM_ACC = 512 / BN;             // accumulator buffers in TMEM's 512 columns
 constexpr int WC = BN / 2;                    // accumulator columns per epilogue warp
-constexpr int WSUB = WC / 32;                 // 32-column sub-chunks per warp per tile
 constexpr int BK = 64;                        // k-block: one 128-byte swizzle row of A
 constexpr int UK = 16;                        // UMMA K for kind::f16
 constexpr int EPI_WARPS = 8;                  // 2 per SMSP; warps w, w+4 share a lane quadrant
@@ -379,7 +378,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     uint32_t chk = 0u;  // NaN-propagating packed max |out| (16-bit) for the non-finite check
     uint32_t rep_loads = 0;
-    int cur_key = -1;   // row-block whose rep tile is in the slot (-1: none)
+    int cur_key = -1;   // row-block whose rep values are in repv (-1: none)
+    uint4 repv[WC / 8];
     int it = 0;
     for (int t = t_begin; t < t_end; ++t, ++it) {
       int pi, m0, n0;
@@ -389,9 +389,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int key = blk_key(pi, m0);
       const bool fast = P.rep_fast != 0;
       if (fast && key != cur_key) {
+        // New row-block: pull this thread's rep values (row row_t, the warp's WC columns
+        // mod d_h — the same for every tile of the row-block) from the staged tile into
+        // registers once, then hand the slot straight back for the next row-block.
         mbar_wait(rfull, rep_loads & 1u);
         ++rep_loads;
         cur_key = key;
+        const int dm = P.d_h - 1;
+#pragma unroll
+        for (int g = 0; g < WC / 8; ++g) {
+          const int jj = (8 * g) & dm;  // warp column base is a multiple of 128
+          const uint32_t ch = static_cast<uint32_t>((jj & 63) >> 3);
+          repv[g] = *reinterpret_cast<const uint4*>(rep_row + (jj >> 6) * REP_BOX +
+                                                    ((ch ^ (row_t & 7)) << 4));
+        }
+        named_bar_sync(2, 32 * EPI_WARPS);  // every epilogue thread holds its rep values
+        if (leader) {
+          for (int tn = t + 1; tn < t_end; ++tn) {  // prefetch the next row-block's rep
+            int npi, nm0, nn0;
+            decode_tile(prm, tn, npi, nm0, nn0);
+            if (blk_key(npi, nm0) != key) {
+              if (prm.p[npi].rep_fast) issue_rep(tn);
+              break;
+            }
+          }
+        }
       }
       const int acc = it % NUM_ACC;
       const uint32_t acc_phase = (it / NUM_ACC) & 1;
@@ -402,46 +424,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint16_t* xrow = static_cast<const uint16_t*>(P.x) +
                              (grow < P.L ? grow : 0) * P.ldx + P.rep_base;
       const int cbase = n0 + static_cast<int>(half) * WC;
-      int nsub = (P.N - cbase + 31) / 32;
-      nsub = nsub < 0 ? 0 : (nsub > WSUB ? WSUB : nsub);
+      int nchunk = (P.N - cbase + 15) / 16;
+      nchunk = nchunk < 0 ? 0 : (nchunk > WC / 16 ? WC / 16 : nchunk);
       const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * BN + half * WC;
-      const int dmask = P.d_h - 1;
 
-      auto process = [&](const uint32_t (&r)[32], int sub) {
-        const int col0 = cbase + sub * 32;
-        uint4 xv[4];
+      // One 16-column chunk c (accumulator registers r): + rep, round, swizzled staging
+      // into the warp's 32 x 64 box (four chunks per box); the box's TMA store is issued
+      // after its fourth chunk (or the tile's last).  Before a box's first chunk is
+      // written, the previous box's store must have finished reading the buffer.
+      auto process = [&](const uint32_t (&r)[16], int c) {
+        const int col0 = cbase + c * 16;
+        uint4 xv[2];
         if (fast) {
-          const int jj0 = col0 & dmask;  // d_h in {64,128}: 32 columns never wrap a head
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const int jj = jj0 + 8 * g;
-            const uint32_t ch = static_cast<uint32_t>((jj & 63) >> 3);
-            xv[g] = *reinterpret_cast<const uint4*>(rep_row + (jj >> 6) * REP_BOX +
-                                                    ((ch ^ (row_t & 7)) << 4));
-          }
+          xv[0] = repv[2 * c];
+          xv[1] = repv[2 * c + 1];
         } else if (!has_rep) {
-#pragma unroll
-          for (int g = 0; g < 4; ++g) xv[g] = make_uint4(0, 0, 0, 0);
+          xv[0] = xv[1] = make_uint4(0, 0, 0, 0);
         } else {
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
+          for (int g = 0; g < 2; ++g) {
             const int col = col0 + 8 * g;
             xv[g] = (col < P.N && grow < P.L)
                         ? __ldg(reinterpret_cast<const uint4*>(xrow + (col % P.d_h)))
                         : make_uint4(0, 0, 0, 0);
           }
         }
-        // Two 32-column sub-chunks fill one 32 x 64 staging box; the box's TMA store is
-        // issued after the second.  Before the first writes, the previous box's store must
-        // have finished reading the buffer (it was issued a whole sub-chunk pair ago).
-        const uint32_t stg = stg0;
-        const uint32_t gpart = static_cast<uint32_t>(sub & 1) * 4;
-        if ((sub & 1) == 0) {
+        const uint32_t q4 = static_cast<uint32_t>(c & 3);
+        if (q4 == 0) {
           if (lane == 0) tma_store_wait_read<0>();
           __syncwarp();
         }
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
+        for (int g = 0; g < 2; ++g) {
           const uint32_t xw[4] = {xv[g].x, xv[g].y, xv[g].z, xv[g].w};
           uint32_t o[4];
 #pragma unroll
@@ -453,39 +467,41 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             o[e] = pack2<kBF16>(v.x, v.y);
             if constexpr (kCheck) chk = max_abs2_nan<kBF16>(chk, o[e]);
           }
-          const uint32_t dst = stg + row_w * 128 + (((gpart + g) ^ sw128) << 4);
+          const uint32_t dst = stg0 + row_w * 128 + (((2 * q4 + g) ^ sw128) << 4);
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(o[0]),
                        "r"(o[1]), "r"(o[2]), "r"(o[3])
                        : "memory");
         }
-        if ((sub & 1) == 1 || sub + 1 == nsub) {
+        if (q4 == 3 || c + 1 == nchunk) {
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             asm volatile(
                 "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                     reinterpret_cast<uint64_t>(&P.map_out)),
-                "r"(stg), "r"(col0 - (sub & 1) * 32), "r"(my_m0 + static_cast<int>(quad) * 32)
+                "r"(stg0), "r"(col0 - static_cast<int>(q4) * 16),
+                "r"(my_m0 + static_cast<int>(quad) * 32)
                 : "memory");
             tma_store_commit();
           }
         }
       };
 
-      if (nsub > 0) {
-        uint32_t ra[32], rb[32];
-        tmem_ld_32x32b_x32(taddr, ra);
+      if (nchunk > 0) {
+        // 16-column TMEM loads, double-buffered: chunk c+1 is in flight while c is processed
+        uint32_t ra[16], rb[16];
+        tmem_ld_32x32b_x16(taddr, ra);
 #pragma unroll
-        for (int sub = 0; sub < WSUB; sub += 2) {
-          if (sub < nsub) {
+        for (int c = 0; c < WC / 16; c += 2) {
+          if (c < nchunk) {
             tmem_ld_wait();
-            if (sub + 1 < nsub) tmem_ld_32x32b_x32(taddr + (sub + 1) * 32, rb);
-            process(ra, sub);
+            if (c + 1 < nchunk) tmem_ld_32x32b_x16(taddr + (c + 1) * 16, rb);
+            process(ra, c);
           }
-          if (sub + 1 < nsub) {
+          if (c + 1 < nchunk) {
             tmem_ld_wait();
-            if (sub + 2 < nsub) tmem_ld_32x32b_x32(taddr + (sub + 2) * 32, ra);
-            process(rb, sub + 1);
+            if (c + 2 < nchunk) tmem_ld_32x32b_x16(taddr + (c + 2) * 16, ra);
+            process(rb, c + 1);
           }
         }
       }
@@ -493,12 +509,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       named_bar_sync(1, 32 * EPI_WARPS);  // all epilogue threads finished with TMEM + rep
       if (leader) {
         mbar_arrive_remote(mapa_shared(smem_u32(&tempty[acc]), 0));
-        // the next tile starts a new row-block: restage the rep slot (nobody reads it now)
-        if (t + 1 < t_end) {
-          int npi, nm0, nn0;
-          decode_tile(prm, t + 1, npi, nm0, nn0);
-          if (prm.p[npi].rep_fast && blk_key(npi, nm0) != cur_key) issue_rep(t + 1);
-        }
       }
     }
     if (lane == 0) tma_store_wait_all<0>();
