@@ -241,6 +241,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: everything above (barrier init, TMEM allocation,
+  // descriptor prefetch) may overlap the tail of the previous kernel in the stream; no
+  // global memory that kernel may write is touched before this wait.  Dependents may
+  // launch right away — they cannot fit on an SM until this CTA exits, and they wait the
+  // same way for this grid's completion before reading its output.
+  griddep_wait();
+  griddep_launch_dependents();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -636,13 +643,19 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  static const bool pdl = [] {  // BD_PDL=0 disables programmatic dependent launch
+    const char* e = getenv("BD_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cg;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm);
   note_launch();
   if (e == cudaSuccess) e = cudaGetLastError();
