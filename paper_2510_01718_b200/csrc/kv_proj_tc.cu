@@ -29,8 +29,12 @@
 //
 // TMEM holds two 128 x 256 FP32 accumulators (all 512 columns): the epilogue of tile i
 // overlaps the MMAs of tile i+1.  The repeated slice x[m0:m0+128, rep_base:+d_h] is
-// staged once per row-block into one smem slot by the epilogue's own leader thread, so
-// the producer never waits on the epilogue.
+// staged once per row-block into one smem slot by the epilogue's leader thread (TMA),
+// read once into registers (a warp's 128 columns map to the same d_h rep columns for
+// every tile of the row-block) and the slot is immediately refilled for the next
+// row-block, so neither the producer nor the epilogue waits on it in steady state.
+// The add is one mixed-precision FHADD (f32 + f16/bf16) per element.  Launches use
+// programmatic dependent launch: the prologue overlaps the previous kernel's tail.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
