@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 TAG=${TAG:-prof}
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e \
+  --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-block \
   > gpurun_out/${TAG}_launches_bench.log 2>&1
 echo "launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:kv_proj_tc -s 2 -c 1 \
