@@ -60,7 +60,6 @@ constexpr int BM = 128;                       // rows per CTA per tile (TMEM lan
 #endif
 constexpr int BN = BD_BN;                     // UMMA N (output columns per pair tile)
 constexpr int NUM_ACC = 512 / BN;             // accumulator buffers in TMEM's 512 columns
-constexpr int WC = BN / 2;                    // accumulator columns per epilogue warp
 constexpr int BK = 64;                        // k-block: one 128-byte swizzle row of A
 constexpr int UK = 16;                        // UMMA K for kind::f16
 constexpr int EPI_WARPS = 8;                  // 2 per SMSP; warps w, w+4 share a lane quadrant
@@ -255,7 +254,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    // Warp-uniform loop (tensor-map / barrier operands stay in uniform registers); one
+    // elected lane issues each TMA.
+    {
       const uint64_t pol = policy_evict_last();  // x and c are re-read; out streams past
       uint32_t a_iter = 0, b_iter = 0;
       int prev_key = -1;
@@ -276,19 +277,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (reload_a) {
             const uint32_t s = a_iter % A_SLOTS;
             mbar_wait(&a_empty[s], ((a_iter / A_SLOTS) & 1u) ^ 1u);
-            if (rank == 0) mbar_arrive_expect_tx(&a_full[s], CG * A_BYTES);
-            tma_load_2d_pair(sA + s * A_BYTES, &P.map_a, kb * BK, my_m0,
-                             mapa_shared(smem_u32(&a_full[s]), 0), pol);
+            if (elect_one()) {
+              if (rank == 0) mbar_arrive_expect_tx(&a_full[s], CG * A_BYTES);
+              tma_load_2d_pair(sA + s * A_BYTES, &P.map_a, kb * BK, my_m0,
+                               mapa_shared(smem_u32(&a_full[s]), 0), pol);
+            }
+            __syncwarp();
             ++a_iter;
           }
           const uint32_t s = b_iter % B_STAGES;
           mbar_wait(&b_empty[s], ((b_iter / B_STAGES) & 1u) ^ 1u);
-          if (rank == 0) mbar_arrive_expect_tx(&b_full[s], CG * B_BYTES);
-          const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), 0);
+          if (elect_one()) {
+            if (rank == 0) mbar_arrive_expect_tx(&b_full[s], CG * B_BYTES);
+            const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), 0);
 #pragma unroll
-          for (int q = 0; q < B_PANELS; ++q)
-            tma_load_2d_pair(sB + s * B_BYTES + q * B_PANEL, &P.map_b, my_n0 + 64 * q, kb * BK,
-                             bar, pol);
+            for (int q = 0; q < B_PANELS; ++q)
+              tma_load_2d_pair(sB + s * B_BYTES + q * B_PANEL, &P.map_b, my_n0 + 64 * q,
+                               kb * BK, bar, pol);
+          }
+          __syncwarp();
           ++b_iter;
         }
       }
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t chk = 0u;  // NaN-propagating packed max |out| (16-bit) for the non-finite check
     uint32_t rep_loads = 0;
     int cur_key = -1;   // row-block whose rep values are in repv (-1: none)
-    uint4 repv[WC / 8];
+    uint4 repv[8];      // rep values of this thread's row, columns half*64 + [0, 64) mod d_h
     int it = 0;
     for (int t = t_begin; t < t_end; ++t, ++it) {
       int pi, m0, n0;
@@ -408,8 +415,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         cur_key = key;
         const int dm = P.d_h - 1;
 #pragma unroll
-        for (int g = 0; g < WC / 8; ++g) {
-          const int jj = (8 * g) & dm;  // warp column base is a multiple of 128
+        for (int g = 0; g < 8; ++g) {
+          const int jj = (static_cast<int>(half) * 64 + 8 * g) & dm;
           const uint32_t ch = static_cast<uint32_t>((jj & 63) >> 3);
           repv[g] = *reinterpret_cast<const uint4*>(rep_row + (jj >> 6) * REP_BOX +
                                                     ((ch ^ (row_t & 7)) << 4));
@@ -434,39 +441,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool has_rep = P.has_rep != 0;
       const uint16_t* xrow = static_cast<const uint16_t*>(P.x) +
                              (grow < P.L ? grow : 0) * P.ldx + P.rep_base;
-      const int cbase = n0 + static_cast<int>(half) * WC;
-      int nchunk = (P.N - cbase + 15) / 16;
-      nchunk = nchunk < 0 ? 0 : (nchunk > WC / 16 ? WC / 16 : nchunk);
-      const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * BN + half * WC;
+      // Warp columns: two 64-wide spans, [64 h, 64 h + 64) and [128 + 64 h, ...) of the
+      // tile (h = half), so both spans map to the same d_h-periodic rep columns (d_h in
+      // {64, 128}) and the rep needs only 32 registers.  Four 32-column sub-chunks c:
+      // column cb(c) = (c >> 1) * 128 + 64 h + (c & 1) * 32 (increasing in c).
+      auto cb = [&](int c) { return (c >> 1) * 128 + static_cast<int>(half) * 64 + (c & 1) * 32; };
+      int nsub = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) nsub += (n0 + cb(c) < P.N) ? 1 : 0;
+      const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * BN;
 
-      // One 16-column chunk c (accumulator registers r): + rep, round, swizzled staging
-      // into the warp's 32 x 64 box (four chunks per box); the box's TMA store is issued
-      // after its fourth chunk (or the tile's last).  Before a box's first chunk is
-      // written, the previous box's store must have finished reading the buffer.
-      auto process = [&](const uint32_t (&r)[16], int c) {
-        const int col0 = cbase + c * 16;
-        uint4 xv[2];
+      // One 32-column sub-chunk c: + rep, round, swizzled staging into the warp's
+      // 32 x 64 box (two sub-chunks per box, one box per span); the box's TMA store is
+      // issued after its second sub-chunk (or the tile's last).  Before a box's first
+      // sub-chunk is written, the previous box's store must have finished reading it.
+      auto process = [&](const uint32_t (&r)[32], int c) {
+        const int col0 = n0 + cb(c);
+        uint4 xv[4];
         if (fast) {
-          xv[0] = repv[2 * c];
-          xv[1] = repv[2 * c + 1];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) xv[g] = repv[(c & 1) * 4 + g];
         } else if (!has_rep) {
-          xv[0] = xv[1] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int g = 0; g < 4; ++g) xv[g] = make_uint4(0, 0, 0, 0);
         } else {
 #pragma unroll
-          for (int g = 0; g < 2; ++g) {
+          for (int g = 0; g < 4; ++g) {
             const int col = col0 + 8 * g;
             xv[g] = (col < P.N && grow < P.L)
                         ? __ldg(reinterpret_cast<const uint4*>(xrow + (col % P.d_h)))
                         : make_uint4(0, 0, 0, 0);
           }
         }
-        const uint32_t q4 = static_cast<uint32_t>(c & 3);
-        if (q4 == 0) {
+        const uint32_t part = static_cast<uint32_t>(c & 1);
+        if (part == 0) {
           if (lane == 0) tma_store_wait_read<0>();
           __syncwarp();
         }
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
+        for (int g = 0; g < 4; ++g) {
           const uint32_t xw[4] = {xv[g].x, xv[g].y, xv[g].z, xv[g].w};
           uint32_t o[4];
 #pragma unroll
@@ -478,19 +491,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             o[e] = pack2<kBF16>(v.x, v.y);
             if constexpr (kCheck) chk = max_abs2_nan<kBF16>(chk, o[e]);
           }
-          const uint32_t dst = stg0 + row_w * 128 + (((2 * q4 + g) ^ sw128) << 4);
+          const uint32_t dst = stg0 + row_w * 128 + (((4 * part + g) ^ sw128) << 4);
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(o[0]),
                        "r"(o[1]), "r"(o[2]), "r"(o[3])
                        : "memory");
         }
-        if (q4 == 3 || c + 1 == nchunk) {
+        if (part == 1 || c + 1 == nsub) {
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             asm volatile(
                 "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                     reinterpret_cast<uint64_t>(&P.map_out)),
-                "r"(stg0), "r"(col0 - static_cast<int>(q4) * 16),
+                "r"(stg0), "r"(col0 - static_cast<int>(part) * 32),
                 "r"(my_m0 + static_cast<int>(quad) * 32)
                 : "memory");
             tma_store_commit();
@@ -498,20 +511,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       };
 
-      if (nchunk > 0) {
-        // 16-column TMEM loads, double-buffered: chunk c+1 is in flight while c is processed
-        uint32_t ra[16], rb[16];
-        tmem_ld_32x32b_x16(taddr, ra);
+      if (nsub > 0) {
+        // 32-column TMEM loads, double-buffered: sub-chunk c+1 is in flight while c is
+        // processed (tcgen05.wait::ld waits for all of a thread's loads, so two is the depth)
+        uint32_t ra[32], rb[32];
+        tmem_ld_32x32b_x32(taddr + cb(0), ra);
 #pragma unroll
-        for (int c = 0; c < WC / 16; c += 2) {
-          if (c < nchunk) {
+        for (int c = 0; c < 4; c += 2) {
+          if (c < nsub) {
             tmem_ld_wait();
-            if (c + 1 < nchunk) tmem_ld_32x32b_x16(taddr + (c + 1) * 16, rb);
+            if (c + 1 < nsub) tmem_ld_32x32b_x32(taddr + cb(c + 1), rb);
             process(ra, c);
           }
-          if (c + 1 < nchunk) {
+          if (c + 1 < nsub) {
             tmem_ld_wait();
-            if (c + 2 < nchunk) tmem_ld_32x32b_x16(taddr + (c + 2) * 16, ra);
+            if (c + 2 < nsub) tmem_ld_32x32b_x32(taddr + cb(c + 2), ra);
             process(rb, c + 1);
           }
         }
