@@ -54,6 +54,17 @@ from .linear import (
     lowrank_forward,
     matmul,
 )
+from .tensorio import (
+    ManifestError,
+    TensorFileError,
+    load_bda_manifest,
+    load_mha_manifest,
+    load_tensor,
+    manifest_kind,
+    save_bda_manifest,
+    save_mha_manifest,
+    save_tensor,
+)
 from .verify import (
     EQUIVALENCE_THRESHOLDS,
     KERNEL_MAXREL,

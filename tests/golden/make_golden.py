@@ -163,8 +163,21 @@ def linear_small() -> None:
     print(f"linear_small: {len(meta)} cases")
 
 
+def bundle() -> None:
+    """A prepared bundle written by the reference's own tensorio (`bdattn prepare`
+    output format): MHA and BDA manifests + BDT1 files for a small seeded model."""
+    from bdattn import tensorio
+    out = OUT / "bundle"
+    out.mkdir(exist_ok=True)
+    w = bd.gen_random_mha(Rng(21), 24, 4, 5, Precision.P32)
+    p = bd.bda_prepare(w, prepare_in_p64=True)
+    tensorio.save_mha_manifest(out / "model.mha", w)
+    tensorio.save_bda_manifest(out / "model.bda", p)
+    print("bundle:", sorted(f.name for f in out.iterdir()))
+
+
 if __name__ == "__main__":
-    fused_small()
-    cfg1()
-    prep_tags()
-    linear_small()
+    import sys as _sys
+    todo = _sys.argv[1:] or ["fused_small", "cfg1", "prep_tags", "linear_small", "bundle"]
+    for name in todo:
+        globals()[name]()

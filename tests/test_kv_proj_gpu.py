@@ -240,3 +240,15 @@ def test_launch_counter_counts_our_kernels(cuda):
     bd.fused_kv_proj(x, c, 32, 2, check_finite=False)
     torch.cuda.synchronize()
     assert N.launch_count() == before + 1
+
+
+def test_compat_shim_is_bit_exact_on_every_reference_case(small, cuda):
+    """INTEGRATION.md's drop-in for numba's _fused_kernel (numpy in, out overwritten)."""
+    from paper_2510_01718_b200 import compat
+    meta, arrs = small
+    for i, m in enumerate(meta):
+        x, c = arrs[f"x{i}"], arrs[f"c{i}"]
+        mul_base, rep_base = O.tag_offsets(x.shape[1], m["d_h"], m["tag"])
+        out = np.zeros((x.shape[0], m["n_heads"] * m["d_h"]), dtype=x.dtype)  # ref pre-zeroes
+        compat._fused_kernel(x, c, m["d_h"], m["n_heads"], mul_base, rep_base, out)
+        np.testing.assert_array_equal(out, arrs[f"out{i}"], err_msg=m["source"])
