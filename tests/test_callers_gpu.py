@@ -145,3 +145,21 @@ def test_matmul_fp16_and_launch_count(cuda):
     assert N.launch_count() == before + 1
     ref = a.double() @ b.double()
     assert bd.max_relative_error(got, ref) <= 1e-3
+
+
+def test_bd_linear_cfg4_geometry_fp16(cuda):
+    """BASELINE config 4 layer (4096 -> 1024 -> 4096), 256 tokens: both GEMMs stream K
+    (4096 and 1024) through the kernel; oracle with h rounded like the kernel."""
+    din, r, dout, L = 4096, 1024, 4096, 256
+    g = torch.Generator().manual_seed(7)
+    basis = (torch.randn(din, r, generator=g) / 64).half()
+    coeff = (torch.randn(r, dout - r, generator=g) / 32).half()
+    fac = bd.BDFactors(axis=bd.Axis.COLUMN, tag=bd.Tag.LAST, basis=basis.double().numpy(),
+                       coeff=coeff.double().numpy(), orig_rows=din, orig_cols=dout, rank=r,
+                       residual=0.0, rank_deficient=False)
+    layer = bd.BDLinearLayer(fac, basis.to(cuda), coeff.to(cuda))
+    x = torch.randn(L, din, generator=g).half().to(cuda)
+    y = bd.bd_linear_forward(x, layer, check_finite=True)
+    h = (x.double() @ basis.to(cuda).double()).half().double()
+    want = torch.cat([h @ coeff.to(cuda).double(), h], dim=1)  # LAST: [h C, h]
+    assert bd.max_relative_error(y, want) <= 2e-3

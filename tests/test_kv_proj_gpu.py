@@ -252,3 +252,36 @@ def test_compat_shim_is_bit_exact_on_every_reference_case(small, cuda):
         out = np.zeros((x.shape[0], m["n_heads"] * m["d_h"]), dtype=x.dtype)  # ref pre-zeroes
         compat._fused_kernel(x, c, m["d_h"], m["n_heads"], mul_base, rep_base, out)
         np.testing.assert_array_equal(out, arrs[f"out{i}"], err_msg=m["source"])
+
+
+def test_tc_cfg3_llama_shape_streaming_k(cuda):
+    """BASELINE config 3 geometry (d=4096, 32 heads x 128, BF16): K = 3968 streams A
+    through the slot ring.  512 tokens, sampled rows vs the FP64 oracle."""
+    L, d, d_h, n = 512, 4096, 128, 32
+    g = torch.Generator().manual_seed(33)
+    x = torch.randn(L, d, generator=g).bfloat16().to(cuda)
+    ck = (torch.randn(d - d_h, n * d_h, generator=g) / 64).bfloat16().to(cuda)
+    cv = (torch.randn(d - d_h, n * d_h, generator=g) / 64).bfloat16().to(cuda)
+    k, v = bd.fused_kv_proj_grouped(x, [(ck, d_h, n, bd.Tag.FIRST), (cv, d_h, n, bd.Tag.LAST)],
+                                    check_finite=True)
+    rows = torch.tensor([0, 1, 127, 128, 255, 256, 300, 511], device=cuda)
+    assert_tc_close(k, x, ck, d_h, n, bd.Tag.FIRST, rows=rows)
+    assert_tc_close(v, x, cv, d_h, n, bd.Tag.LAST, rows=rows)
+
+
+def test_tc_grouped_four_problems_mixed_shapes(cuda):
+    """Up to BD_MAX_GROUP problems in one launch, different N / d_h / tags and one
+    resident-A (K <= 384) next to one streaming-A (K > 384) problem."""
+    g = torch.Generator().manual_seed(44)
+    L = 300
+    x1 = torch.randn(L, 512, generator=g).half().to(cuda)
+    c1 = (torch.randn(384, 2048, generator=g) / 8).half().to(cuda)
+    c2 = (torch.randn(448, 512, generator=g) / 8).half().to(cuda)
+    c3 = (torch.randn(384, 256, generator=g) / 8).half().to(cuda)
+    c4 = (torch.randn(504, 64, generator=g) / 8).half().to(cuda)
+    outs = bd.fused_kv_proj_grouped(x1, [(c1, 128, 16, bd.Tag.FIRST), (c2, 64, 8, bd.Tag.LAST),
+                                         (c3, 128, 2, bd.Tag.LAST), (c4, 8, 8, bd.Tag.FIRST)])
+    for o, (c, d_h, n, tag) in zip(outs, [(c1, 128, 16, bd.Tag.FIRST), (c2, 64, 8, bd.Tag.LAST),
+                                          (c3, 128, 2, bd.Tag.LAST), (c4, 8, 8, bd.Tag.FIRST)]):
+        assert_tc_close(o, x1, c, d_h, n, tag)
+        torch.testing.assert_close(o, bd.fused_kv_proj(x1, c, d_h, n, tag), rtol=0, atol=0)
