@@ -159,35 +159,72 @@ def fused_kv_proj_grouped(x: torch.Tensor,
     return results
 
 
-_staging: dict = {}
+class _HostPipeline:
+    """Per-device streams, events and staging buffers of the chunked host path."""
+
+    def __init__(self, dev):
+        self.h2d = torch.cuda.Stream(dev)
+        self.comp = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        self.bufs: dict = {}
+
+    def buf(self, tag, shape, dtype, dev):
+        key = (tag, tuple(shape), dtype)
+        b = self.bufs.get(key)
+        if b is None:
+            b = self.bufs[key] = torch.empty(shape, dtype=dtype, device=dev)
+        return b
+
+
+_pipes: dict = {}
 
 
 def fused_kv_proj_grouped_host(x_host: torch.Tensor,
                                specs: Sequence[tuple[torch.Tensor, int, int, Tag]],
                                *, outs: Sequence[torch.Tensor] | None = None,
-                               mode: str = "auto") -> list[torch.Tensor]:
+                               mode: str = "auto", chunks: int = 4) -> list[torch.Tensor]:
     """Grouped projection of a HOST activation tensor against device-resident C's.
 
-    Copies x in (H2D, asynchronous when x is pinned), runs the grouped kernel, copies
-    every projection out (D2H into ``outs``, pinned host tensors, or new ones) and
-    synchronises, so the returned host tensors are ready — the end-to-end path of a
-    caller whose activations live on the host.
+    The end-to-end path of a caller whose activations live on the host: copies x in,
+    runs the grouped kernel, copies every projection out (into ``outs``, pinned host
+    tensors, or new pinned ones) and returns once they are ready.  The tokens are split
+    into ``chunks`` row blocks pipelined over three streams — H2D of block i+1, the
+    kernel on block i and D2H of block i-1 overlap — so the step costs about the
+    PCIe transfer of its outputs (the kernel itself is ~1/40 of that at cfg2).
     """
     if x_host.is_cuda:
         raise ValueError("x_host must be a host tensor; use fused_kv_proj_grouped")
     dev = specs[0][0].device
-    key = (dev, tuple(x_host.shape), x_host.dtype)
-    xd = _staging.get(key)
-    if xd is None:
-        xd = _staging[key] = torch.empty(x_host.shape, dtype=x_host.dtype, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    xd.copy_(x_host, non_blocking=True)
-    res = fused_kv_proj_grouped(xd, specs, mode=mode)
+    pipe = _pipes.get(dev)
+    if pipe is None:
+        pipe = _pipes[dev] = _HostPipeline(dev)
+    L = int(x_host.shape[0])
+    xd = pipe.buf("x", x_host.shape, x_host.dtype, dev)
+    dev_outs = [pipe.buf(("o", i), (L, n * d_h), x_host.dtype, dev)
+                for i, (_, d_h, n, _) in enumerate(specs)]
     if outs is None:
-        outs = [torch.empty(r.shape, dtype=r.dtype, pin_memory=True) for r in res]
-    for o, r in zip(outs, res):
-        o.copy_(r, non_blocking=True)
-    stream.synchronize()
+        outs = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in dev_outs]
+    caller = torch.cuda.current_stream(dev)
+    pipe.h2d.wait_stream(caller)  # device buffers are free once the caller's work is
+    step = max(1, -(-L // max(1, chunks)))
+    step = -(-step // 256) * 256  # whole 256-row CTA-pair tiles per block
+    done = None
+    for r0 in range(0, L, step):
+        r1 = min(L, r0 + step)
+        with torch.cuda.stream(pipe.h2d):
+            xd[r0:r1].copy_(x_host[r0:r1], non_blocking=True)
+        pipe.comp.wait_stream(pipe.h2d)
+        with torch.cuda.stream(pipe.comp):
+            fused_kv_proj_grouped(xd[r0:r1], specs, outs=[o[r0:r1] for o in dev_outs], mode=mode)
+        pipe.d2h.wait_stream(pipe.comp)
+        with torch.cuda.stream(pipe.d2h):
+            for o, r in zip(outs, dev_outs):
+                o[r0:r1].copy_(r[r0:r1], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(pipe.d2h)
+    if done is not None:
+        done.synchronize()
+    caller.wait_stream(pipe.d2h)
     return list(outs)
 
 
