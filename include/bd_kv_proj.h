@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define BD_KV_PROJ_ABI_VERSION 2
+#define BD_KV_PROJ_ABI_VERSION 3
 
 /* element types */
 enum bd_dtype { BD_F32 = 0, BD_F64 = 1, BD_F16 = 2, BD_BF16 = 3 };
@@ -61,6 +61,13 @@ enum bd_mode {
   BD_MODE_AUTO = 0,   /* F32/F64 -> exact, F16/BF16 -> tensor core */
   BD_MODE_EXACT = 1,  /* SIMT, reference rounding order (F32/F64 only) */
   BD_MODE_TC = 2      /* tcgen05 tensor cores (F16/BF16 only) */
+};
+
+/* output layouts */
+enum bd_out_layout {
+  BD_OUT_TOKEN_MAJOR = 0, /* out[i, h*d_h + j] at out + i*ldo + h*d_h + j (the reference's) */
+  BD_OUT_HEAD_MAJOR = 1   /* out[h][i][j] at out + (h*L + i)*ldo + j: per-head contiguous,
+                             what per-head attention and a flat head all-gather consume */
 };
 
 /* tags (ref: decompose.py:27-31) */
@@ -133,6 +140,14 @@ int bd_linear_forward(const void* x, int64_t ldx, const void* basis, int64_t ldb
                       const void* coeff, int64_t ldc, void* y, int64_t ldy, int64_t L,
                       int64_t d_in, int64_t rank, int64_t d_out, int tag, int dtype, int mode,
                       int* nonfinite_flag, void* stream);
+
+/*
+ * bd_kv_proj_grouped with an output layout (enum bd_out_layout).  For
+ * BD_OUT_HEAD_MAJOR each problem's out is [n_heads][L][d_h] with row stride ldo >= d_h
+ * (head stride L * ldo).  The tensor-core path needs d_h to be a multiple of 64 there.
+ */
+int bd_kv_proj_grouped_ex(const bd_kv_problem* problems, int count, int dtype, int mode,
+                          int out_layout, int* nonfinite_flag, void* stream);
 
 /* Human-readable description of the last error on this thread ("" if none). */
 const char* bd_last_error(void);

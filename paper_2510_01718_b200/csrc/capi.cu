@@ -59,7 +59,8 @@ int resolve_mode(int dtype, int mode, int* out_mode) {
   return fail(BD_ERR_ARG, "unknown mode " + std::to_string(mode));
 }
 
-int validate(const bd_kv_problem& p, int dtype, int mode, int idx) {
+int validate(const bd_kv_problem& p, int dtype, int mode, int idx,
+             int out_layout = BD_OUT_TOKEN_MAJOR) {
   char buf[256];
   const std::string at = "problem " + std::to_string(idx) + ": ";
   if (p.x == nullptr || p.c == nullptr || p.out == nullptr)
@@ -81,13 +82,19 @@ int validate(const bd_kv_problem& p, int dtype, int mode, int idx) {
              (long long)p.mul_base, (long long)p.rep_base, (long long)p.d, (long long)p.d_h);
     return fail(BD_ERR_SHAPE, at + buf);
   }
-  if (p.ldx < p.d || p.ldc < N || p.ldo < N) {
+  const int64_t min_ldo = out_layout == BD_OUT_HEAD_MAJOR ? p.d_h : N;
+  if (p.ldx < p.d || p.ldc < N || p.ldo < min_ldo) {
     snprintf(buf, sizeof(buf), "row strides too small (ldx=%lld ldc=%lld ldo=%lld, d=%lld N=%lld)",
              (long long)p.ldx, (long long)p.ldc, (long long)p.ldo, (long long)p.d, (long long)N);
     return fail(BD_ERR_SHAPE, at + buf);
   }
   if (p.L > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
     return fail(BD_ERR_SHAPE, at + "dimension exceeds int32 range");
+  if (mode == BD_MODE_TC && out_layout == BD_OUT_HEAD_MAJOR && (p.d_h % 64) != 0) {
+    snprintf(buf, sizeof(buf), "head-major tensor-core output needs d_h %% 64 == 0 (d_h=%lld)",
+             (long long)p.d_h);
+    return fail(BD_ERR_ALIGN, at + buf);
+  }
   if (mode == BD_MODE_TC) {
     if (!aligned16(p.x) || !aligned16(p.c) || !aligned16(p.out))
       return fail(BD_ERR_ALIGN, at + "tensor-core path needs 16-byte aligned x, c and out");
@@ -104,9 +111,9 @@ int validate(const bd_kv_problem& p, int dtype, int mode, int idx) {
   return BD_OK;
 }
 
-Problem to_problem(const bd_kv_problem& q) {
+Problem to_problem(const bd_kv_problem& q, int out_layout) {
   return Problem{q.x, q.c, q.out, q.ldx, q.ldc, q.ldo, q.L, q.d - q.d_h, q.n_heads * q.d_h,
-                 q.d_h, q.mul_base, q.rep_base};
+                 q.d_h, q.mul_base, q.rep_base, out_layout};
 }
 
 int dispatch(const Problem* probs, int count, int dtype, int m, int* flag, cudaStream_t stream) {
@@ -121,7 +128,9 @@ int dispatch(const Problem* probs, int count, int dtype, int m, int* flag, cudaS
 }
 
 int run_group(const bd_kv_problem* probs, int count, int dtype, int mode, int* flag,
-              cudaStream_t stream) {
+              cudaStream_t stream, int out_layout = BD_OUT_TOKEN_MAJOR) {
+  if (out_layout != BD_OUT_TOKEN_MAJOR && out_layout != BD_OUT_HEAD_MAJOR)
+    return fail(BD_ERR_ARG, "unknown out_layout " + std::to_string(out_layout));
   if (probs == nullptr || count < 1 || count > BD_MAX_GROUP)
     return fail(BD_ERR_ARG, "problem count must be in [1, " + std::to_string(BD_MAX_GROUP) + "]");
   if (elem_size(dtype) == 0) return fail(BD_ERR_DTYPE, "unknown dtype " + std::to_string(dtype));
@@ -130,9 +139,9 @@ int run_group(const bd_kv_problem* probs, int count, int dtype, int mode, int* f
   if (rc != BD_OK) return rc;
   Problem ps[BD_MAX_GROUP];
   for (int i = 0; i < count; ++i) {
-    rc = validate(probs[i], dtype, m, i);
+    rc = validate(probs[i], dtype, m, i, out_layout);
     if (rc != BD_OK) return rc;
-    ps[i] = to_problem(probs[i]);
+    ps[i] = to_problem(probs[i], out_layout);
   }
   return dispatch(ps, count, dtype, m, flag, stream);
 }
@@ -218,6 +227,12 @@ int bd_kv_proj_grouped(const bd_kv_problem* problems, int count, int dtype, int 
                         static_cast<cudaStream_t>(stream));
 }
 
+int bd_kv_proj_grouped_ex(const bd_kv_problem* problems, int count, int dtype, int mode,
+                          int out_layout, int* nonfinite_flag, void* stream) {
+  return bdk::run_group(problems, count, dtype, mode, nonfinite_flag,
+                        static_cast<cudaStream_t>(stream), out_layout);
+}
+
 int bd_kv_proj_host(const void* x, const void* c, void* out, int64_t L, int64_t d, int64_t d_h,
                     int64_t n_heads, int64_t mul_base, int64_t rep_base, int dtype, int mode,
                     int* nonfinite) {
@@ -279,7 +294,7 @@ int bd_matmul(const void* a, int64_t lda, const void* b, int64_t ldb, void* out,
   if (rc != BD_OK) return rc;
   rc = validate_matmul(a, lda, b, ldb, out, ldo, M, K, N, m, "bd_matmul");
   if (rc != BD_OK) return rc;
-  Problem p{a, b, out, lda, ldb, ldo, M, K, N, 1, 0, -1};
+  Problem p{a, b, out, lda, ldb, ldo, M, K, N, 1, 0, -1, BD_OUT_TOKEN_MAJOR};
   return dispatch(&p, 1, dtype, m, nonfinite_flag, static_cast<cudaStream_t>(stream));
 }
 
@@ -311,10 +326,10 @@ int bd_linear_forward(const void* x, int64_t ldx, const void* basis, int64_t ldb
                        "bd_linear_forward h C");
   if (rc != BD_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  Problem p1{x, basis, h, ldx, ldb, ldy, L, d_in, rank, 1, 0, -1};
+  Problem p1{x, basis, h, ldx, ldb, ldy, L, d_in, rank, 1, 0, -1, BD_OUT_TOKEN_MAJOR};
   rc = dispatch(&p1, 1, dtype, m, nonfinite_flag, s);
   if (rc != BD_OK) return rc;
-  Problem p2{h, coeff, hc, ldy, ldc, ldy, L, rank, d_out - rank, 1, 0, -1};
+  Problem p2{h, coeff, hc, ldy, ldc, ldy, L, rank, d_out - rank, 1, 0, -1, BD_OUT_TOKEN_MAJOR};
   return dispatch(&p2, 1, dtype, m, nonfinite_flag, s);
 }
 

@@ -122,7 +122,10 @@ __global__ void __launch_bounds__(EX_THREADS)
       if (col >= N) continue;
       const T v = has_rep ? ExactOps<T>::add(acc[i][j], x[row * P.ldx + P.rep_base + (col % P.d_h)])
                           : acc[i][j];
-      out[row * P.ldo + col] = v;
+      if (P.out_layout == BD_OUT_HEAD_MAJOR)
+        out[((col / P.d_h) * P.L + row) * P.ldo + col % P.d_h] = v;
+      else
+        out[row * P.ldo + col] = v;
       bad |= !isfinite(v);
     }
   }

@@ -22,6 +22,8 @@ struct Problem {
   int64_t d_h;       // head width of the repeated slice (ignored without rep)
   int64_t mul_base;  // first multiplied column of x
   int64_t rep_base;  // first repeated column of x; < 0: no repeated-slice add
+  int32_t out_layout;  // BD_OUT_TOKEN_MAJOR (L x N, row stride ldo) or BD_OUT_HEAD_MAJOR
+                       // ([N / d_h][L][d_h], row stride ldo, head stride L * ldo)
 };
 
 // Thread-local error text set by the launchers; returned by bd_last_error().

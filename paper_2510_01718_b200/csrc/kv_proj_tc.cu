@@ -86,13 +86,16 @@ struct TcProblem {
   CUtensorMap map_a;    // x + mul_base, dims {K, L},   box {64, 128}
   CUtensorMap map_b;    // c,            dims {N, K},   box {64, 64}
   CUtensorMap map_rep;  // x + rep_base, dims {d_h, L}, box {64, 128}   (rep_fast only)
-  CUtensorMap map_out;  // out,          dims {N, L},   box {64, 32}, SW128
+  CUtensorMap map_out;  // out: token-major dims {N, L}, box {64, 32}; head-major dims
+                        // {d_h, L, n_heads}, box {64, 32, 1} (clips per head); SW128
   const void* x;
   int64_t ldx;
   int32_t L, N, K, d_h, rep_base;
   int32_t tiles_n, num_kb, tile_start;
   int32_t has_rep;      // 0: plain GEMM (no repeated-slice add)
   int32_t rep_fast;     // d_h in {64, 128}: rep tile staged in smem by TMA
+  int32_t head_major;   // output layout [n_heads][L][d_h]
+  int32_t out_d_h;      // head width of the head-major output
 };
 
 struct TcParams {
@@ -500,12 +503,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            asm volatile(
-                "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                    reinterpret_cast<uint64_t>(&P.map_out)),
-                "r"(stg0), "r"(col0 - static_cast<int>(part) * 32),
-                "r"(my_m0 + static_cast<int>(quad) * 32)
-                : "memory");
+            const int bcol = col0 - static_cast<int>(part) * 32;
+            const int brow = my_m0 + static_cast<int>(quad) * 32;
+            if (P.head_major)
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                      reinterpret_cast<uint64_t>(&P.map_out)),
+                  "r"(stg0), "r"(bcol % P.out_d_h), "r"(brow), "r"(bcol / P.out_d_h)
+                  : "memory");
+            else
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                      reinterpret_cast<uint64_t>(&P.map_out)),
+                  "r"(stg0), "r"(bcol), "r"(brow)
+                  : "memory");
             tma_store_commit();
           }
         }
@@ -593,6 +604,34 @@ bool encode_2d(CUtensorMap* map, const void* base, bool bf16, uint64_t cols, uin
   return true;
 }
 
+// Row-major [planes x rows x cols] 16-bit tensor (row stride ld, plane stride ps
+// elements), box {box_cols, box_rows, 1}, 128B swizzle.
+bool encode_3d(CUtensorMap* map, const void* base, bool bf16, uint64_t cols, uint64_t rows,
+               uint64_t planes, uint64_t ld, uint64_t ps, uint32_t box_cols, uint32_t box_rows,
+               std::string* err) {
+  auto fn = encode_fn();
+  if (fn == nullptr) {
+    *err = "cuTensorMapEncodeTiled unavailable from the driver";
+    return false;
+  }
+  const cuuint64_t dims[3] = {cols, rows, planes};
+  const cuuint64_t strides[2] = {ld * 2, ps * 2};
+  const cuuint32_t box[3] = {box_cols, box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                  3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled (3-D) failed (CUresult %d)",
+             static_cast<int>(r));
+    *err = buf;
+    return false;
+  }
+  return true;
+}
+
 }  // namespace tc
 
 int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_t stream) {
@@ -617,13 +656,18 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
     const auto* xr = static_cast<const uint16_t*>(q.x) + rep_base;
     if (!encode_2d(&P.map_a, xb, bf16, K, q.L, q.ldx, BK, BM, &err) ||
         !encode_2d(&P.map_b, q.c, bf16, N, K, q.ldc, 64, BK, &err) ||
-        !encode_2d(&P.map_out, q.out, bf16, N, q.L, q.ldo, 64, 32, &err) ||
+        !(q.out_layout == BD_OUT_HEAD_MAJOR
+              ? encode_3d(&P.map_out, q.out, bf16, q.d_h, q.L, N / q.d_h, q.ldo, q.L * q.ldo, 64,
+                          32, &err)
+              : encode_2d(&P.map_out, q.out, bf16, N, q.L, q.ldo, 64, 32, &err)) ||
         (rep_fast && !encode_2d(&P.map_rep, xr, bf16, d_h, q.L, q.ldx, 64, BM, &err))) {
       set_error(err);
       return BD_ERR_CUDA;
     }
     P.rep_fast = rep_fast ? 1 : 0;
     P.has_rep = has_rep ? 1 : 0;
+    P.head_major = q.out_layout == BD_OUT_HEAD_MAJOR ? 1 : 0;
+    P.out_d_h = static_cast<int32_t>(q.d_h);
     P.x = q.x;
     P.ldx = q.ldx;
     P.L = static_cast<int32_t>(q.L);

@@ -80,11 +80,33 @@ def _rowmajor(t: torch.Tensor) -> torch.Tensor:
     return t if (t.stride(1) == 1 and t.stride(0) >= t.shape[1]) else t.contiguous()
 
 
+_LAYOUTS = {"token": N.BD_OUT_TOKEN_MAJOR, "head": N.BD_OUT_HEAD_MAJOR}
+
+
+def _out_tensor(x, d_h, n_heads, layout, out=None):
+    """Allocate or validate the output: token-major (L, n d_h) like the reference, or
+    head-major (n, L, d_h) — per-head contiguous, what attention and a flat head
+    all-gather consume."""
+    L = int(x.shape[0])
+    if layout not in _LAYOUTS:
+        raise ValueError(f"unknown out_layout {layout!r}")
+    shape = (L, n_heads * d_h) if layout == "token" else (n_heads, L, d_h)
+    if out is None:
+        return torch.empty(shape, dtype=x.dtype, device=x.device)
+    ok = tuple(out.shape) == shape and out.dtype == x.dtype and out.stride(-1) == 1
+    if layout == "head":
+        ok = ok and out.stride(0) == L * out.stride(1)
+    if not ok:
+        raise ShapeError(f"out must be a {layout}-major {shape} tensor of x's dtype")
+    return out
+
+
 def _problem(x, c, out, d_h, n_heads, tag) -> N.KvProblem:
     L, d = int(x.shape[0]), int(x.shape[1])
     mul_base, rep_base = tag_offsets(d, d_h, tag)
+    ldo = out.stride(0) if out.dim() == 2 else out.stride(1)
     return N.KvProblem(x.data_ptr(), c.data_ptr(), out.data_ptr(), x.stride(0), c.stride(0),
-                       out.stride(0), L, d, d_h, n_heads, mul_base, rep_base)
+                       ldo, L, d, d_h, n_heads, mul_base, rep_base)
 
 
 def _finish(flag: torch.Tensor | None) -> None:
@@ -94,7 +116,8 @@ def _finish(flag: torch.Tensor | None) -> None:
 
 def fused_kv_proj(x: torch.Tensor, c: torch.Tensor, d_h: int, n_heads: int,
                   tag: Tag = Tag.FIRST, *, out: torch.Tensor | None = None,
-                  check_finite: bool = True, mode: str = "auto") -> torch.Tensor:
+                  check_finite: bool = True, mode: str = "auto",
+                  out_layout: str = "token") -> torch.Tensor:
     """Merged key/value projection in one pass over the output.
 
     Equivalent to tiling one d_h-wide slice of x n_heads times and adding the
@@ -106,17 +129,15 @@ def fused_kv_proj(x: torch.Tensor, c: torch.Tensor, d_h: int, n_heads: int,
     _check(x, c, d_h, n_heads)
     x = _rowmajor(x)
     c = _rowmajor(c)
-    L = int(x.shape[0])
-    if out is None:
-        out = torch.empty((L, n_heads * d_h), dtype=x.dtype, device=x.device)
-    elif out.shape != (L, n_heads * d_h) or out.dtype != x.dtype or out.stride(1) != 1:
-        raise ShapeError("out must be a row-major (L, n_heads*d_h) tensor of x's dtype")
+    out = _out_tensor(x, d_h, n_heads, out_layout, out)
     flag = torch.zeros(1, dtype=torch.int32, device=x.device) if check_finite else None
     prob = _problem(x, c, out, d_h, n_heads, tag)
     stream = torch.cuda.current_stream(x.device).cuda_stream
     with torch.cuda.device(x.device):
-        st = N.load().bd_kv_proj_grouped(ctypes.byref(prob), 1, _DTYPES[x.dtype], _MODES[mode],
-                                         flag.data_ptr() if flag is not None else None, stream)
+        st = N.load().bd_kv_proj_grouped_ex(ctypes.byref(prob), 1, _DTYPES[x.dtype],
+                                            _MODES[mode], _LAYOUTS[out_layout],
+                                            flag.data_ptr() if flag is not None else None,
+                                            stream)
     N.check(st, "bd_kv_proj")
     _finish(flag)
     return out
@@ -126,7 +147,8 @@ def fused_kv_proj_grouped(x: torch.Tensor,
                           specs: Sequence[tuple[torch.Tensor, int, int, Tag]],
                           *, outs: Sequence[torch.Tensor] | None = None,
                           check_finite: bool = False, mode: str = "auto",
-                          flag: torch.Tensor | None = None) -> list[torch.Tensor]:
+                          flag: torch.Tensor | None = None,
+                          out_layout: str = "token") -> list[torch.Tensor]:
     """Several projections of the same x in ONE kernel launch.
 
     ``specs`` is a list of (c, d_h, n_heads, tag) — e.g. K' and V' of
@@ -140,10 +162,7 @@ def fused_kv_proj_grouped(x: torch.Tensor,
     for i, (c, d_h, n_heads, tag) in enumerate(specs):
         _check(x, c, d_h, n_heads)
         c = _rowmajor(c)
-        if outs is not None:
-            o = outs[i]
-        else:
-            o = torch.empty((x.shape[0], n_heads * d_h), dtype=x.dtype, device=x.device)
+        o = _out_tensor(x, d_h, n_heads, out_layout, outs[i] if outs is not None else None)
         probs[i] = _problem(x, c, o, d_h, n_heads, tag)
         results.append(o)
     own_flag = flag is None and check_finite
@@ -151,8 +170,10 @@ def fused_kv_proj_grouped(x: torch.Tensor,
         flag = torch.zeros(1, dtype=torch.int32, device=x.device)
     stream = torch.cuda.current_stream(x.device).cuda_stream
     with torch.cuda.device(x.device):
-        st = N.load().bd_kv_proj_grouped(probs, len(specs), _DTYPES[x.dtype], _MODES[mode],
-                                         flag.data_ptr() if flag is not None else None, stream)
+        st = N.load().bd_kv_proj_grouped_ex(probs, len(specs), _DTYPES[x.dtype], _MODES[mode],
+                                            _LAYOUTS[out_layout],
+                                            flag.data_ptr() if flag is not None else None,
+                                            stream)
     N.check(st, "bd_kv_proj_grouped")
     if own_flag:
         _finish(flag)

@@ -81,19 +81,30 @@ GPU_OPS = Ops()
 
 
 def sharded_kv_proj(x: torch.Tensor, c_local: torch.Tensor, d_h: int, tag: Tag,
-                    *, ops: Ops = GPU_OPS) -> torch.Tensor:
-    """This rank's heads of K' (token-major [L, n_local d_h]); no collective."""
+                    *, ops: Ops = GPU_OPS, head_major: bool = False) -> torch.Tensor:
+    """This rank's heads of K'; no collective.  Token-major [L, n_local d_h], or with
+    ``head_major`` the kernel writes [n_local, L, d_h] directly (per-head contiguous:
+    what head-parallel attention and ``all_gather_heads`` consume without a copy)."""
     n_local = c_local.shape[1] // d_h
+    if head_major:
+        return ops.kv_proj_grouped(x, [(c_local, d_h, n_local, tag)], out_layout="head")[0]
     return ops.kv_proj_grouped(x, [(c_local, d_h, n_local, tag)])[0]
 
 
 def all_gather_heads(local: torch.Tensor, d_h: int, group=None) -> torch.Tensor:
-    """Full-width [L, n d_h] from every rank's [L, n_local d_h], heads in rank order.
+    """Full width from every rank's heads, heads in rank order.
 
     One ``all_gather_into_tensor`` over the head-major layout: each rank contributes a
-    contiguous [n_local, L, d_h] block, so the collective is a single flat gather.
+    contiguous [n_local, L, d_h] block, so the collective is a single flat gather.  A
+    head-major local (3-D, straight from the kernel) gathers without any copy and
+    returns [n, L, d_h]; a token-major local is staged and [L, n d_h] returned.
     """
     world = dist.get_world_size(group)
+    if local.dim() == 3:  # already head-major from the kernel: gather in place, no copy
+        n_local, L, _ = local.shape
+        full = torch.empty((world * n_local, L, d_h), dtype=local.dtype, device=local.device)
+        dist.all_gather_into_tensor(full, local, group=group)
+        return full
     L, w = local.shape
     n_local = w // d_h
     head_major = local.view(L, n_local, d_h).permute(1, 0, 2).contiguous()

@@ -285,3 +285,30 @@ def test_tc_grouped_four_problems_mixed_shapes(cuda):
                                           (c3, 128, 2, bd.Tag.LAST), (c4, 8, 8, bd.Tag.FIRST)]):
         assert_tc_close(o, x1, c, d_h, n, tag)
         torch.testing.assert_close(o, bd.fused_kv_proj(x1, c, d_h, n, tag), rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("shape", [(300, 512, 128, 16), (77, 256, 64, 3), (8192, 512, 128, 16)])
+def test_head_major_output_equals_token_major(dtype, shape, cuda):
+    """out_layout='head' writes [n, L, d_h] (per-head TMA boxes clipped at each head's
+    L rows): bit-identical to the token-major result rearranged."""
+    L, d, d_h, n = shape
+    g = torch.Generator().manual_seed(L + d_h)
+    x = torch.randn(L, d, generator=g).to(dtype).to(cuda)
+    ck = (torch.randn(d - d_h, n * d_h, generator=g) / 8).to(dtype).to(cuda)
+    cv = (torch.randn(d - d_h, n * d_h, generator=g) / 8).to(dtype).to(cuda)
+    specs = [(ck, d_h, n, bd.Tag.FIRST), (cv, d_h, n, bd.Tag.LAST)]
+    tok = bd.fused_kv_proj_grouped(x, specs)
+    head = bd.fused_kv_proj_grouped(x, specs, out_layout="head")
+    for t, h in zip(tok, head):
+        assert h.shape == (n, L, d_h)
+        torch.testing.assert_close(h, t.view(L, n, d_h).permute(1, 0, 2), rtol=0, atol=0)
+    single = bd.fused_kv_proj(x, cv, d_h, n, bd.Tag.LAST, out_layout="head")
+    torch.testing.assert_close(single, head[1], rtol=0, atol=0)
+
+
+def test_head_major_tc_needs_d_h_multiple_of_64(cuda):
+    x = torch.randn(64, 72, device=cuda).half()
+    c = torch.randn(64, 16, device=cuda).half()
+    with pytest.raises(bd.ShapeError):
+        bd.fused_kv_proj(x, c, 8, 2, out_layout="head")

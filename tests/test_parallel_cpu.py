@@ -36,10 +36,13 @@ def cpu_ops():
     sys.path.insert(0, str(ROOT))
     from oracle import oracle as O
 
-    def kv(x, specs):
+    def kv(x, specs, out_layout="token"):
         outs = []
         for c, d_h, n, tag in specs:
-            outs.append(torch.from_numpy(O.fused_kv_proj_ref(x.numpy(), c.numpy(), d_h, n, tag.value)))
+            o = torch.from_numpy(O.fused_kv_proj_ref(x.numpy(), c.numpy(), d_h, n, tag.value))
+            if out_layout == "head":
+                o = o.view(-1, n, d_h).permute(1, 0, 2).contiguous()
+            outs.append(o)
         return outs
 
     def proj(x, w):
@@ -81,6 +84,12 @@ def _worker(rank, world, port, q):
             assert local.shape == (256, 8 // w * 64)
             full = P.all_gather_heads(local, 64)
             res[name] = hashlib.sha256(full.numpy().tobytes()).hexdigest()
+            # head-major straight from the kernel: gathered with no staging copy
+            hm = P.sharded_kv_proj(x, P.shard_columns(c, 64, 8, w, r), 64, bd.Tag(tag), ops=ops,
+                                   head_major=True)
+            fh = P.all_gather_heads(hm, 64)
+            assert fh.shape == (8, 256, 64)
+            assert torch.equal(fh.permute(1, 0, 2).reshape(256, 512), full)
         # --- block: global prep, then shard; compare with the unsharded block
         mha = bd.gen_random_mha(bd.Rng(3), 48, 8, 4, torch.float64)
         prepared = bd.bda_prepare(mha)
