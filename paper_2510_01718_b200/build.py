@@ -22,7 +22,6 @@ SOURCES = ["capi.cu", "kv_proj_exact.cu", "kv_proj_tc.cu"]
 HEADERS = ["ptx_sm100.cuh", "kv_proj_internal.h"]
 
 NVCC_FLAGS = [
-    *([f"-DBD_DEV_KNOBS=1"] if os.environ.get("BD_DEV_KNOBS") else []),
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared",

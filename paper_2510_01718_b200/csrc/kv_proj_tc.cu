@@ -55,19 +55,14 @@ namespace tc {
 
 constexpr int CG = 2;                         // cta_group::2 (CTA pairs)
 constexpr int BM = 128;                       // rows per CTA per tile (TMEM lanes)
-#ifndef BD_BN
-#define BD_BN 256
-#endif
-constexpr int BN = BD_BN;                     // UMMA N (output columns per pair tile)
+constexpr int BN = 256;                       // UMMA N (output columns per pair tile)
 constexpr int NUM_ACC = 512 / BN;             // accumulator buffers in TMEM's 512 columns
+static_assert(BN == 256, "the epilogue's column mapping assumes 256-wide tiles");
 constexpr int BK = 64;                        // k-block: one 128-byte swizzle row of A
 constexpr int UK = 16;                        // UMMA K for kind::f16
 constexpr int EPI_WARPS = 8;                  // 2 per SMSP; warps w, w+4 share a lane quadrant
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
-#ifndef BD_A_SLOTS
-#define BD_A_SLOTS 6
-#endif
-constexpr int A_SLOTS = BD_A_SLOTS;           // resident A: K <= 6 * 64 = 384
+constexpr int A_SLOTS = 6;                    // resident A: K <= 6 * 64 = 384
 constexpr int B_STAGES = 4;
 constexpr uint32_t A_BYTES = BM * BK * 2;     // 16 KiB: 128 rows x 64 k
 constexpr uint32_t B_PANEL = 64 * BK * 2;     // one 64-column MN-major swizzle panel, 8 KiB
