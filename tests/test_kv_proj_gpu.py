@@ -134,6 +134,8 @@ TC_SHAPES = [
     (128, 328, 64, 3),      # K=264 (not a multiple of 64), N=192 (< one 256 tile)
     (77, 136, 8, 5),        # tiny d_h, N=40
     (300, 1024, 128, 7),    # N = 896: last tile partial
+    (200, 1024, 256, 3),    # d_h = 256: rep not staged (per-element gather path), K = 768
+    (130, 200, 24, 5),      # d_h = 24, N = 120: odd head width, one partial sub-chunk
 ]
 
 
