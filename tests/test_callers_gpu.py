@@ -163,3 +163,17 @@ def test_bd_linear_cfg4_geometry_fp16(cuda):
     h = (x.double() @ basis.to(cuda).double()).half().double()
     want = torch.cat([h @ coeff.to(cuda).double(), h], dim=1)  # LAST: [h C, h]
     assert bd.max_relative_error(y, want) <= 2e-3
+
+
+def test_head_sharded_bda_partials_sum_to_the_full_block(cuda):
+    """parallel.sharded_bda_forward on one device: the shards' partial outputs (no
+    process group -> no all_reduce) sum to the unsharded bda_forward."""
+    from paper_2510_01718_b200 import parallel as P
+    w = bd.gen_random_mha(bd.Rng(12), 48, 8, 6, torch.float64)
+    prepared = bd.bda_prepare(w).to(cuda)
+    x = bd.rand_gaussian(bd.Rng(13), 25, 48, torch.float64, cuda)
+    full = bd.bda_forward(x, prepared, causal=True)
+    for world in (2, 3, 6):
+        parts = [P.sharded_bda_forward(x, P.shard_bda_weights(prepared, world, r), causal=True)
+                 for r in range(world)]
+        assert bd.max_relative_error(sum(parts), full) <= 1e-12

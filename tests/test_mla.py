@@ -86,3 +86,18 @@ def test_bd_mla_dsv2_lite_fp16_vs_fp64_dense(cuda):
     print(f"DSV2-Lite block 2048 tok FP16 max-rel vs FP64 dense: BD {e_bd:.3g}, dense {e_dense:.3g}")
     assert torch.isfinite(got16).all()
     assert e_bd <= 0.1  # measured 2.95e-2 (dense FP16: 6.6e-4), B200 round 1
+
+
+@pytest.mark.gpu
+def test_head_sharded_mla_partials_sum_to_the_full_block(cuda):
+    """cfg5's multi-GPU split on one device: each head shard's partial block output
+    (its q columns, C columns, B_vo rows; kv_a replicated) sums to the unsharded block —
+    what the all_reduce in bd_mla_forward computes across ranks."""
+    w = M.gen_random_mla(8, SMALL)
+    p = M.mla_prepare(w).to(cuda)
+    hid = torch.randn(33, SMALL.hidden, dtype=torch.float64,
+                      generator=torch.Generator().manual_seed(9)).to(cuda)
+    full = M.bd_mla_forward(hid, p)
+    for world in (2, 4):
+        parts = [M.bd_mla_forward(hid, M.shard_bd_mla(p, world, r)) for r in range(world)]
+        assert bd.max_relative_error(sum(parts), full) <= 1e-12
