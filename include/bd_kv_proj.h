@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define BD_KV_PROJ_ABI_VERSION 3
+#define BD_KV_PROJ_ABI_VERSION 4
 
 /* element types */
 enum bd_dtype { BD_F32 = 0, BD_F64 = 1, BD_F16 = 2, BD_BF16 = 3 };
@@ -148,6 +148,21 @@ int bd_linear_forward(const void* x, int64_t ldx, const void* basis, int64_t ldb
  */
 int bd_kv_proj_grouped_ex(const bd_kv_problem* problems, int count, int dtype, int mode,
                           int out_layout, int* nonfinite_flag, void* stream);
+
+/*
+ * Head-parallel projection with the all-gather FUSED into the epilogue: this rank owns
+ * n_heads heads of each problem and writes them, head-major, straight into every rank's
+ * full-width buffer over NVLink (peer pointers, e.g. torch symmetric memory), so no
+ * separate collective runs after the kernel.  For problem p, gathered[p*world + r] is
+ * rank r's [world*n_heads][L][d_h] buffer (row stride problems[p].ldo >= d_h); this
+ * rank's heads land in planes [rank*n_heads, (rank+1)*n_heads) of each.  problems[p].out
+ * is ignored.  world in [1, BD_MAX_PEERS].  The caller must order the peers' reads after
+ * every rank's kernel (a barrier on the stream).  Tensor-core path: d_h % 64 == 0.
+ */
+#define BD_MAX_PEERS 8
+int bd_kv_proj_grouped_allgather(const bd_kv_problem* problems, int count, int dtype, int mode,
+                                 int world, int rank, void* const* gathered,
+                                 int* nonfinite_flag, void* stream);
 
 /* Human-readable description of the last error on this thread ("" if none). */
 const char* bd_last_error(void);

@@ -113,7 +113,7 @@ int validate(const bd_kv_problem& p, int dtype, int mode, int idx,
 
 Problem to_problem(const bd_kv_problem& q, int out_layout) {
   return Problem{q.x, q.c, q.out, q.ldx, q.ldc, q.ldo, q.L, q.d - q.d_h, q.n_heads * q.d_h,
-                 q.d_h, q.mul_base, q.rep_base, out_layout};
+                 q.d_h, q.mul_base, q.rep_base, out_layout, 0, 0, {}};
 }
 
 int dispatch(const Problem* probs, int count, int dtype, int m, int* flag, cudaStream_t stream) {
@@ -128,7 +128,8 @@ int dispatch(const Problem* probs, int count, int dtype, int m, int* flag, cudaS
 }
 
 int run_group(const bd_kv_problem* probs, int count, int dtype, int mode, int* flag,
-              cudaStream_t stream, int out_layout = BD_OUT_TOKEN_MAJOR) {
+              cudaStream_t stream, int out_layout = BD_OUT_TOKEN_MAJOR, int world = 0,
+              int rank = 0, void* const* gathered = nullptr) {
   if (out_layout != BD_OUT_TOKEN_MAJOR && out_layout != BD_OUT_HEAD_MAJOR)
     return fail(BD_ERR_ARG, "unknown out_layout " + std::to_string(out_layout));
   if (probs == nullptr || count < 1 || count > BD_MAX_GROUP)
@@ -142,6 +143,17 @@ int run_group(const bd_kv_problem* probs, int count, int dtype, int mode, int* f
     rc = validate(probs[i], dtype, m, i, out_layout);
     if (rc != BD_OK) return rc;
     ps[i] = to_problem(probs[i], out_layout);
+    if (world > 0) {
+      ps[i].world = world;
+      ps[i].head0 = static_cast<int32_t>(rank * probs[i].n_heads);
+      for (int r = 0; r < world; ++r) {
+        ps[i].peers[r] = gathered[i * world + r];
+        if (ps[i].peers[r] == nullptr) return fail(BD_ERR_ARG, "null gathered buffer");
+        if (m == BD_MODE_TC && !aligned16(ps[i].peers[r]))
+          return fail(BD_ERR_ALIGN, "gathered buffers must be 16-byte aligned");
+      }
+      ps[i].out = ps[i].peers[rank];
+    }
   }
   return dispatch(ps, count, dtype, m, flag, stream);
 }
@@ -233,6 +245,25 @@ int bd_kv_proj_grouped_ex(const bd_kv_problem* problems, int count, int dtype, i
                         static_cast<cudaStream_t>(stream), out_layout);
 }
 
+int bd_kv_proj_grouped_allgather(const bd_kv_problem* problems, int count, int dtype, int mode,
+                                 int world, int rank, void* const* gathered,
+                                 int* nonfinite_flag, void* stream) {
+  using namespace bdk;
+  if (world < 1 || world > BD_MAX_PEERS || rank < 0 || rank >= world)
+    return fail(BD_ERR_ARG, "world must be in [1, BD_MAX_PEERS] and 0 <= rank < world");
+  if (gathered == nullptr) return fail(BD_ERR_ARG, "null gathered pointer array");
+  if (problems == nullptr || count < 1 || count > BD_MAX_GROUP)
+    return fail(BD_ERR_ARG, "problem count must be in [1, " + std::to_string(BD_MAX_GROUP) + "]");
+  // out is ignored: point it at this rank's buffer so the shared validation passes
+  bd_kv_problem local[BD_MAX_GROUP];
+  for (int i = 0; i < count; ++i) {
+    local[i] = problems[i];
+    local[i].out = gathered[i * world + rank];
+  }
+  return run_group(local, count, dtype, mode, nonfinite_flag, static_cast<cudaStream_t>(stream),
+                   BD_OUT_HEAD_MAJOR, world, rank, gathered);
+}
+
 int bd_kv_proj_host(const void* x, const void* c, void* out, int64_t L, int64_t d, int64_t d_h,
                     int64_t n_heads, int64_t mul_base, int64_t rep_base, int dtype, int mode,
                     int* nonfinite) {
@@ -294,7 +325,7 @@ int bd_matmul(const void* a, int64_t lda, const void* b, int64_t ldb, void* out,
   if (rc != BD_OK) return rc;
   rc = validate_matmul(a, lda, b, ldb, out, ldo, M, K, N, m, "bd_matmul");
   if (rc != BD_OK) return rc;
-  Problem p{a, b, out, lda, ldb, ldo, M, K, N, 1, 0, -1, BD_OUT_TOKEN_MAJOR};
+  Problem p{a, b, out, lda, ldb, ldo, M, K, N, 1, 0, -1, BD_OUT_TOKEN_MAJOR, 0, 0, {}};
   return dispatch(&p, 1, dtype, m, nonfinite_flag, static_cast<cudaStream_t>(stream));
 }
 
@@ -326,10 +357,11 @@ int bd_linear_forward(const void* x, int64_t ldx, const void* basis, int64_t ldb
                        "bd_linear_forward h C");
   if (rc != BD_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  Problem p1{x, basis, h, ldx, ldb, ldy, L, d_in, rank, 1, 0, -1, BD_OUT_TOKEN_MAJOR};
+  Problem p1{x, basis, h, ldx, ldb, ldy, L, d_in, rank, 1, 0, -1, BD_OUT_TOKEN_MAJOR, 0, 0, {}};
   rc = dispatch(&p1, 1, dtype, m, nonfinite_flag, s);
   if (rc != BD_OK) return rc;
-  Problem p2{h, coeff, hc, ldy, ldc, ldy, L, rank, d_out - rank, 1, 0, -1, BD_OUT_TOKEN_MAJOR};
+  Problem p2{h, coeff, hc, ldy, ldc, ldy, L, rank, d_out - rank, 1, 0, -1, BD_OUT_TOKEN_MAJOR,
+             0, 0, {}};
   return dispatch(&p2, 1, dtype, m, nonfinite_flag, s);
 }
 

@@ -122,10 +122,14 @@ __global__ void __launch_bounds__(EX_THREADS)
       if (col >= N) continue;
       const T v = has_rep ? ExactOps<T>::add(acc[i][j], x[row * P.ldx + P.rep_base + (col % P.d_h)])
                           : acc[i][j];
-      if (P.out_layout == BD_OUT_HEAD_MAJOR)
+      if (P.world > 0) {  // fused all-gather: every rank's full-width head-major buffer
+        const int64_t off = ((P.head0 + col / P.d_h) * P.L + row) * P.ldo + col % P.d_h;
+        for (int r = 0; r < P.world; ++r) static_cast<T*>(P.peers[r])[off] = v;
+      } else if (P.out_layout == BD_OUT_HEAD_MAJOR) {
         out[((col / P.d_h) * P.L + row) * P.ldo + col % P.d_h] = v;
-      else
+      } else {
         out[row * P.ldo + col] = v;
+      }
       bad |= !isfinite(v);
     }
   }

@@ -24,6 +24,11 @@ struct Problem {
   int64_t rep_base;  // first repeated column of x; < 0: no repeated-slice add
   int32_t out_layout;  // BD_OUT_TOKEN_MAJOR (L x N, row stride ldo) or BD_OUT_HEAD_MAJOR
                        // ([N / d_h][L][d_h], row stride ldo, head stride L * ldo)
+  // Fused all-gather (world > 0): head-major output written to every peer buffer
+  // peers[r] ([world * N / d_h][L][d_h]) at head planes [head0, head0 + N / d_h).
+  int32_t world;
+  int32_t head0;
+  void* peers[BD_MAX_PEERS];
 };
 
 // Thread-local error text set by the launchers; returned by bd_last_error().

@@ -95,6 +95,11 @@ struct TcProblem {
 
 struct TcParams {
   TcProblem p[BD_MAX_GROUP];
+  // fused all-gather: per problem, the head-major 3-D map {d_h, L, world * n_heads} of
+  // every rank's gathered buffer (peer memory over NVLink); world == 0 otherwise
+  CUtensorMap map_peer[BD_MAX_GROUP][BD_MAX_PEERS];
+  int32_t world;
+  int32_t head0[BD_MAX_GROUP];
   int32_t count;
   int32_t total_tiles;  // tiles of (BM * CG) rows x BN columns
   int* flag;            // non-finite flag (kCheck instantiation only)
@@ -500,7 +505,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (lane == 0) {
             const int bcol = col0 - static_cast<int>(part) * 32;
             const int brow = my_m0 + static_cast<int>(quad) * 32;
-            if (P.head_major)
+            if (prm.world > 0) {
+              // all-gather fused into the epilogue: the same staged box goes to every
+              // rank's full-width buffer, at this rank's head planes
+              for (int r = 0; r < prm.world; ++r)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                        reinterpret_cast<uint64_t>(&prm.map_peer[pi][r])),
+                    "r"(stg0), "r"(bcol % P.out_d_h), "r"(brow),
+                    "r"(prm.head0[pi] + bcol / P.out_d_h)
+                    : "memory");
+            } else if (P.head_major)
               asm volatile(
                   "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                       reinterpret_cast<uint64_t>(&P.map_out)),
@@ -662,6 +677,17 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
     P.rep_fast = rep_fast ? 1 : 0;
     P.has_rep = has_rep ? 1 : 0;
     P.head_major = q.out_layout == BD_OUT_HEAD_MAJOR ? 1 : 0;
+    if (q.world > 0) {
+      prm.world = q.world;
+      prm.head0[i] = q.head0;
+      for (int r = 0; r < q.world; ++r)
+        if (!encode_3d(&prm.map_peer[i][r], q.peers[r], bf16, q.d_h, q.L,
+                       static_cast<uint64_t>(q.world) * (N / q.d_h), q.ldo, q.L * q.ldo, 64, 32,
+                       &err)) {
+          set_error(err);
+          return BD_ERR_CUDA;
+        }
+    }
     P.out_d_h = static_cast<int32_t>(q.d_h);
     P.x = q.x;
     P.ldx = q.ldx;

@@ -32,9 +32,12 @@ from typing import Callable
 import torch
 import torch.distributed as dist
 
+import ctypes
+
+from . import _native as N
 from .attention import BDAWeights, _attend, _proj
 from .decompose import Tag
-from .kv_proj import fused_kv_proj_grouped
+from .kv_proj import _DTYPES, _MODES, _check, _problem, _rowmajor, fused_kv_proj_grouped
 
 
 def head_range(n_heads: int, world: int, rank: int) -> tuple[int, int]:
@@ -113,6 +116,67 @@ def all_gather_heads(local: torch.Tensor, d_h: int, group=None) -> torch.Tensor:
     return full.permute(1, 0, 2).reshape(L, world * n_local * d_h)
 
 
+def fused_allgather_kv_proj(x: torch.Tensor,
+                            specs: list[tuple[torch.Tensor, int, int, Tag]],
+                            gathered: list[list[torch.Tensor]], rank: int, *,
+                            mode: str = "auto") -> None:
+    """Head-parallel projection with the all-gather fused into the kernel's epilogue.
+
+    ``specs`` are this rank's (c_local, d_h, n_local, tag) problems; ``gathered[p][r]`` is
+    rank r's full-width head-major buffer [world * n_local, L, d_h] for problem p — peer
+    memory (``SymmetricGather`` below) on a multi-GPU node, any device tensors for a
+    single-device check.  The kernel writes this rank's heads into planes
+    [rank * n_local, (rank + 1) * n_local) of EVERY buffer over NVLink as it produces
+    them (TMA stores to peer addresses), so the transfer overlaps the math tile by tile
+    and no NCCL collective follows.  Readers must synchronise with all ranks afterwards
+    (``SymmetricGather.barrier``).
+    """
+    world = len(gathered[0])
+    if not 1 <= world <= N.BD_MAX_PEERS or not 0 <= rank < world:
+        raise ValueError(f"world must be in [1, {N.BD_MAX_PEERS}] and 0 <= rank < world")
+    x = _rowmajor(x)
+    L = int(x.shape[0])
+    probs = (N.KvProblem * len(specs))()
+    ptrs = (ctypes.c_void_p * (len(specs) * world))()
+    for i, (c, d_h, n, tag) in enumerate(specs):
+        _check(x, c, d_h, n)
+        c = _rowmajor(c)
+        for r, g in enumerate(gathered[i]):
+            if tuple(g.shape) != (world * n, L, d_h) or g.dtype != x.dtype or not g.is_contiguous():
+                raise ValueError(f"gathered[{i}][{r}] must be a contiguous {(world * n, L, d_h)} "
+                                 f"{x.dtype} tensor")
+            ptrs[i * world + r] = g.data_ptr()
+        probs[i] = _problem(x, c, gathered[i][rank][rank * n:(rank + 1) * n], d_h, n, tag)
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    with torch.cuda.device(x.device):
+        st = N.load().bd_kv_proj_grouped_allgather(probs, len(specs), _DTYPES[x.dtype],
+                                                   _MODES[mode], world, rank, ptrs, None, stream)
+    N.check(st, "bd_kv_proj_grouped_allgather")
+
+
+class SymmetricGather:
+    """Per-problem full-width gather buffers in torch symmetric memory (one allocation
+    per rank, peer-mapped over NVLink) for ``fused_allgather_kv_proj``."""
+
+    def __init__(self, shapes: list[tuple[int, int, int]], dtype, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        self.group = group if group is not None else dist.group.WORLD
+        self.rank = dist.get_rank(self.group)
+        self.world = dist.get_world_size(self.group)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.local, self.handles, self.peers = [], [], []
+        for shape in shapes:
+            buf = symm_mem.empty(shape, dtype=dtype, device=dev)
+            hdl = symm_mem.rendezvous(buf, self.group)
+            self.local.append(buf)
+            self.handles.append(hdl)
+            self.peers.append([hdl.get_buffer(r, shape, dtype) for r in range(self.world)])
+
+    def barrier(self) -> None:
+        """Every rank's writes into every buffer are complete and visible."""
+        self.handles[0].barrier()
+
+
 def sharded_bda_forward(x: torch.Tensor, w_local: BDAWeights, *, causal: bool = False,
                         group=None, ops: Ops = GPU_OPS) -> torch.Tensor:
     """BDA block with heads sharded over the group: local Q', K', V' (K' and V' in one
@@ -157,5 +221,5 @@ def flops_per_rank(L: int, d: int, d_h: int, n_heads: int, world: int) -> int:
 
 
 __all__ = ["head_range", "shard_columns", "shard_bda_weights", "Ops", "GPU_OPS",
-           "sharded_kv_proj", "all_gather_heads", "sharded_bda_forward", "init_from_env",
-           "weak_scaling_tokens", "flops_per_rank"]
+           "sharded_kv_proj", "all_gather_heads", "fused_allgather_kv_proj", "SymmetricGather",
+           "sharded_bda_forward", "init_from_env", "weak_scaling_tokens", "flops_per_rank"]

@@ -314,3 +314,29 @@ def test_head_major_tc_needs_d_h_multiple_of_64(cuda):
     c = torch.randn(64, 16, device=cuda).half()
     with pytest.raises(bd.ShapeError):
         bd.fused_kv_proj(x, c, 8, 2, out_layout="head")
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_fused_allgather_single_device_ranks(dtype, world, cuda):
+    """The all-gather fused into the epilogue, every 'rank' on one device: after each
+    rank's launch with its head shard, EVERY rank's gathered buffer holds the full
+    head-major K'/V' — bit-identical to the unsharded head-major projection (the
+    multi-GPU version differs only in the buffers being peer memory)."""
+    from paper_2510_01718_b200 import parallel as P
+    L, d, d_h, n = 700, 512, 128, 16
+    g = torch.Generator().manual_seed(world)
+    x = torch.randn(L, d, generator=g).to(dtype).to(cuda)
+    ck = (torch.randn(d - d_h, n * d_h, generator=g) / 8).to(dtype).to(cuda)
+    cv = (torch.randn(d - d_h, n * d_h, generator=g) / 8).to(dtype).to(cuda)
+    full = bd.fused_kv_proj_grouped(x, [(ck, d_h, n, bd.Tag.FIRST), (cv, d_h, n, bd.Tag.LAST)],
+                                    out_layout="head")
+    gathered = [[torch.full((n, L, d_h), 3.0, dtype=dtype, device=cuda) for _ in range(world)]
+                for _ in range(2)]
+    for r in range(world):
+        specs = [(P.shard_columns(ck, d_h, n, world, r), d_h, n // world, bd.Tag.FIRST),
+                 (P.shard_columns(cv, d_h, n, world, r), d_h, n // world, bd.Tag.LAST)]
+        P.fused_allgather_kv_proj(x, specs, gathered, r)
+    for p_ in range(2):
+        for r in range(world):
+            torch.testing.assert_close(gathered[p_][r], full[p_], rtol=0, atol=0)
