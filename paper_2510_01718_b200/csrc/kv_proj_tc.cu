@@ -58,14 +58,16 @@ constexpr int BM = 128;                       // rows per CTA per tile (TMEM lan
 constexpr int BN = 256;                       // UMMA N (output columns per pair tile)
 constexpr int NUM_ACC = 512 / BN;             // accumulator buffers in TMEM's 512 columns
 static_assert(BN == 256, "the epilogue's column mapping assumes 256-wide tiles");
-constexpr int BK = 64;                        // k-block: one 128-byte swizzle row of A
+constexpr int BK = 64;                        // A k-block: one 128-byte swizzle row of A
+constexpr int BKB = 64;                       // B k-block (BKB = 32 with 8 stages: +4 us)
+constexpr int B_SUB = BK / BKB;               // B stages per A k-block
 constexpr int UK = 16;                        // UMMA K for kind::f16
 constexpr int EPI_WARPS = 8;                  // 2 per SMSP; warps w, w+4 share a lane quadrant
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int A_SLOTS = 6;                    // resident A: K <= 6 * 64 = 384
 constexpr int B_STAGES = 4;
 constexpr uint32_t A_BYTES = BM * BK * 2;     // 16 KiB: 128 rows x 64 k
-constexpr uint32_t B_PANEL = 64 * BK * 2;     // one 64-column MN-major swizzle panel, 8 KiB
+constexpr uint32_t B_PANEL = 64 * BKB * 2;    // one 64-column MN-major swizzle panel, 4 KiB
 constexpr int B_PANELS = (BN / 64) / CG;      // this CTA's half of the B tile: 2 panels
 constexpr uint32_t B_BYTES = B_PANELS * B_PANEL;
 constexpr uint32_t REP_BOX = 64 * BM * 2;     // one 64-column x 128-row rep box, 16 KiB
@@ -74,19 +76,20 @@ constexpr uint32_t STG_BYTES = 32 * 64 * 2;   // output staging box: 32 rows x 6
 constexpr int STG_BUFS = 1;                   // per-warp staging buffers
 constexpr uint32_t TMEM_COLS = 512;          // NUM_ACC accumulator buffers
 constexpr size_t SMEM_BYTES = 1024 + A_SLOTS * A_BYTES + B_STAGES * B_BYTES + REP_BYTES +
-                              EPI_WARPS * STG_BUFS * STG_BYTES + 256;
+                              EPI_WARPS * STG_BUFS * STG_BYTES + 512;
+static_assert((2 * A_SLOTS + 2 * B_STAGES + 2 * NUM_ACC + 1) * 8 + 4 <= 512, "barrier area");
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
 struct TcProblem {
   CUtensorMap map_a;    // x + mul_base, dims {K, L},   box {64, 128}
-  CUtensorMap map_b;    // c,            dims {N, K},   box {64, 64}
+  CUtensorMap map_b;    // c,            dims {N, K},   box {64, BKB}
   CUtensorMap map_rep;  // x + rep_base, dims {d_h, L}, box {64, 128}   (rep_fast only)
   CUtensorMap map_out;  // out: token-major dims {N, L}, box {64, 32}; head-major dims
                         // {d_h, L, n_heads}, box {64, 32, 1} (clips per head); SW128
   const void* x;
   int64_t ldx;
   int32_t L, N, K, d_h, rep_base;
-  int32_t tiles_n, num_kb, tile_start;
+  int32_t tiles_n, num_kb, num_kbb, tile_start;  // num_kbb: B k-blocks (BKB deep)
   int32_t has_rep;      // 0: plain GEMM (no repeated-slice add)
   int32_t rep_fast;     // d_h in {64, 128}: rep tile staged in smem by TMA
   int32_t head_major;   // output layout [n_heads][L][d_h]
@@ -112,6 +115,42 @@ __device__ __forceinline__ void decode_tile(const TcParams& prm, int t, int& pi,
   const int local = t - prm.p[pi].tile_start;
   n0 = (local % prm.p[pi].tiles_n) * BN;
   m0 = (local / prm.p[pi].tiles_n) * (BM * CG);
+}
+
+// Sequential walk over a pair's contiguous tile range without per-tile divisions
+// (decode_tile once, then carry (problem, m0, n0) forward).  The MMA issuer's tile
+// boundary sits on the tensor pipe's critical path: a full decode there (integer
+// division + indexed parameter loads) cost ~700 clocks per tile.
+struct TileCursor {
+  int pi, m0, n0;
+  int n_span;    // tiles_n * BN of problem pi
+  int pend;      // first tile of problem pi + 1
+  int t;
+};
+__device__ __forceinline__ void cursor_load(const TcParams& prm, TileCursor& c) {
+  c.n_span = prm.p[c.pi].tiles_n * BN;
+  c.pend = c.pi + 1 < prm.count ? prm.p[c.pi + 1].tile_start : 0x7fffffff;
+}
+__device__ __forceinline__ TileCursor cursor_at(const TcParams& prm, int t) {
+  TileCursor c;
+  c.t = t;
+  decode_tile(prm, t, c.pi, c.m0, c.n0);
+  cursor_load(prm, c);
+  return c;
+}
+__device__ __forceinline__ void cursor_next(const TcParams& prm, TileCursor& c) {
+  ++c.t;
+  c.n0 += BN;
+  if (c.n0 >= c.n_span) {
+    c.n0 = 0;
+    c.m0 += BM * CG;
+  }
+  if (c.t >= c.pend) {
+    ++c.pi;
+    c.m0 = 0;
+    c.n0 = 0;
+    cursor_load(prm, c);
+  }
 }
 
 // Tiles sharing (problem, pair row-block) share the A row-block and the rep tile.
@@ -272,12 +311,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         prev_key = key;
         const int my_m0 = m0 + static_cast<int>(rank) * BM;
         const int my_n0 = n0 + static_cast<int>(rank) * (BN / CG);
-        for (int kb = 0; kb < P.num_kb; ++kb) {
+        for (int j = 0; j < P.num_kbb; ++j) {
+          const int kb = j / B_SUB;
           // Both CTAs' bytes complete on the LEADER's barriers, which the leader arms with
           // the pair's total.  The peer does not arrive: the barrier cannot complete
           // before the leader's arrival, and each CTA only refills a slot after the
           // multicast commit released it, i.e. after the previous phase completed.
-          if (reload_a) {
+          if (reload_a && j % B_SUB == 0) {
             const uint32_t s = a_iter % A_SLOTS;
             mbar_wait(&a_empty[s], ((a_iter / A_SLOTS) & 1u) ^ 1u);
             if (elect_one()) {
@@ -296,7 +336,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int q = 0; q < B_PANELS; ++q)
               tma_load_2d_pair(sB + s * B_BYTES + q * B_PANEL, &P.map_b, my_n0 + 64 * q,
-                               kb * BK, bar, pol);
+                               j * BKB, bar, pol);
           }
           __syncwarp();
           ++b_iter;
@@ -313,34 +353,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t a_iter = 0, a_base = 0, b_iter = 0;
       int prev_key = -1;
       int it = 0;
+      TileCursor cur = cursor_at(prm, t_begin);
+      TileCursor nxt = cur;
+      cursor_next(prm, nxt);
       for (int t = t_begin; t < t_end; ++t, ++it) {
-        int pi, m0, n0;
-        decode_tile(prm, t, pi, m0, n0);
+        const int pi = cur.pi;
         const TcProblem& P = prm.p[pi];
-        const int key = blk_key(pi, m0);
-        const bool stream_a = P.num_kb > A_SLOTS;
+        const int num_kb = P.num_kb, num_kbb = P.num_kbb;
+        const int key = blk_key(pi, cur.m0);
+        const bool stream_a = num_kb > A_SLOTS;
         const bool reload_a = stream_a || key != prev_key;
         prev_key = key;
         // Last tile reading this A row-block: release each slot after its k-block's MMAs.
-        bool last_use = true;
-        if (!stream_a && t + 1 < t_end) {
-          int npi, nm0, nn0;
-          decode_tile(prm, t + 1, npi, nm0, nn0);
-          last_use = blk_key(npi, nm0) != key;
-        }
+        const bool last_use = stream_a || t + 1 >= t_end || blk_key(nxt.pi, nxt.m0) != key;
+        cur = nxt;
+        cursor_next(prm, nxt);
         if (reload_a) {
           a_base = a_iter;
-          a_iter += P.num_kb;
+          a_iter += num_kb;
         }
         const int acc = it % NUM_ACC;
         const uint32_t acc_phase = (it / NUM_ACC) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < P.num_kb; ++kb) {
+        for (int j = 0; j < num_kbb; ++j) {
+          const int kb = j / B_SUB;
           const uint32_t ai = a_base + kb;
           const uint32_t as = ai % A_SLOTS;
-          if (reload_a) mbar_wait(&a_full[as], (ai / A_SLOTS) & 1u);
+          if (reload_a && j % B_SUB == 0) mbar_wait(&a_full[as], (ai / A_SLOTS) & 1u);
           const uint32_t bs = b_iter % B_STAGES;
           mbar_wait(&b_full[bs], (b_iter / B_STAGES) & 1u);
           tc_fence_after();
@@ -348,17 +389,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t b0 = smem_u32(sB + bs * B_BYTES);
           if (elect_one()) {
 #pragma unroll
-            for (int ks = 0; ks < BK / UK; ++ks) {
+            for (int ks = 0; ks < BKB / UK; ++ks) {
               // A: K-major SW128, rows 128 B apart, 8-row groups 1024 B apart; a 16-wide
               //    k step is +32 B inside the swizzle row.
-              const uint64_t adesc = make_smem_desc(a0 + ks * (UK * 2), 16, 1024);
+              const uint64_t adesc =
+                  make_smem_desc(a0 + ((j % B_SUB) * BKB + ks * UK) * 2, 16, 1024);
               // B: MN-major SW128, 64-column panels B_PANEL apart (LBO), 8-k-row groups
               //    1024 B apart (SBO); a 16-deep k step is two 8-row groups = 2048 B.
               const uint64_t bdesc = make_smem_desc(b0 + ks * (UK * 128), B_PANEL, 1024);
-              tc_mma_f16_pair(d_tmem, adesc, bdesc, idesc, (kb | ks) != 0 ? 1u : 0u);
+              tc_mma_f16_pair(d_tmem, adesc, bdesc, idesc, (j | ks) != 0 ? 1u : 0u);
             }
             tc_commit_pair(&b_empty[bs], 0x3);
-            if (last_use) tc_commit_pair(&a_empty[as], 0x3);
+            if (last_use && (j % B_SUB == B_SUB - 1 || j + 1 == num_kbb))
+              tc_commit_pair(&a_empty[as], 0x3);
           }
           __syncwarp();
           ++b_iter;
@@ -665,7 +708,7 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
     const bool rep_fast = has_rep && (d_h % 64 == 0) && d_h <= 128;
     const auto* xr = static_cast<const uint16_t*>(q.x) + rep_base;
     if (!encode_2d(&P.map_a, xb, bf16, K, q.L, q.ldx, BK, BM, &err) ||
-        !encode_2d(&P.map_b, q.c, bf16, N, K, q.ldc, 64, BK, &err) ||
+        !encode_2d(&P.map_b, q.c, bf16, N, K, q.ldc, 64, BKB, &err) ||
         !(q.out_layout == BD_OUT_HEAD_MAJOR
               ? encode_3d(&P.map_out, q.out, bf16, q.d_h, q.L, N / q.d_h, q.ldo, q.L * q.ldo, 64,
                           32, &err)
@@ -698,6 +741,7 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
     P.rep_base = static_cast<int32_t>(rep_base);
     P.tiles_n = static_cast<int32_t>((N + BN - 1) / BN);
     P.num_kb = static_cast<int32_t>((K + BK - 1) / BK);
+    P.num_kbb = static_cast<int32_t>((K + BKB - 1) / BKB);
     P.tile_start = total;
     total += P.tiles_n * static_cast<int32_t>((q.L + BM * cg - 1) / (BM * cg));
   }

@@ -1,0 +1,76 @@
+"""Development aid: write exp/kv_proj_tc_tl.cu — the TC kernel with per-CTA clock stamps
+(globaltimer + clock64 into a __device__ table read back by bd_debug_timeline) for
+tools/timeline.py.  Build:  cd paper_2510_01718_b200/csrc && nvcc <build flags> -I. \
+    -o ../../exp/tl.so capi.cu kv_proj_exact.cu ../../exp/kv_proj_tc_tl.cu"""
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+s = (ROOT / "paper_2510_01718_b200/csrc/kv_proj_tc.cu").read_text()
+
+
+def rep(a, b):
+    global s
+    assert s.count(a) == 1, a[:70]
+    s = s.replace(a, b)
+
+
+i = s.index("namespace bdk {")
+s = (s[:i] + "__device__ unsigned long long g_tl[148][64];\n"
+     + '#define GT() ({unsigned long long _g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_g)); _g;})\n'
+     + "#define CK() ((unsigned long long)clock64())\n" + s[i:])
+s += '''
+extern "C" int bd_debug_timeline(unsigned long long* dst) {
+  return (int)cudaMemcpyFromSymbol(dst, g_tl, sizeof(g_tl));
+}
+'''
+rep('''  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();''', '''  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  unsigned long long* TL = g_tl[blockIdx.x];
+  if (threadIdx.x == 0) { TL[0] = GT(); TL[1] = CK(); }''')
+rep('''    for (int s = 0; s < A_SLOTS; ++s) {
+      mbar_init(&a_full[s], 1);''', '''    TL[2] = CK();
+    for (int s = 0; s < A_SLOTS; ++s) {
+      mbar_init(&a_full[s], 1);''')
+rep('''    mbar_init(rfull, 1);
+    fence_mbar_init();''', '''    mbar_init(rfull, 1);
+    fence_mbar_init();
+    TL[3] = CK();''')
+rep('''    tmem_relinquish<CG>();
+  }''', '''    tmem_relinquish<CG>();
+    if (lane == 0) TL[4] = CK();
+  }''')
+rep('''  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;''', '''  tc_fence_after();
+  if (threadIdx.x == 0) TL[5] = CK();
+  const uint32_t tmem_base = *tmem_slot;''')
+rep('''  griddep_wait();
+  griddep_launch_dependents();
+''', '''  griddep_wait();
+  griddep_launch_dependents();
+  if (threadIdx.x == 0) TL[6] = CK();
+''')
+rep('''            const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), 0);''', '''            const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), 0);
+            if (b_iter == 0) TL[7] = CK();''')
+rep('''        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();''', '''        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        if (lane == 0 && it < 8) TL[8 + it] = CK();
+        unsigned long long bw = 0;''')
+rep('''          mbar_wait(&b_full[bs], (b_iter / B_STAGES) & 1u);''', '''          const unsigned long long w0 = CK();
+          mbar_wait(&b_full[bs], (b_iter / B_STAGES) & 1u);
+          bw += CK() - w0;''')
+rep('''        if (elect_one()) tc_commit_pair(&tfull[acc], 0x3);
+        __syncwarp();''', '''        if (elect_one()) tc_commit_pair(&tfull[acc], 0x3);
+        __syncwarp();
+        if (lane == 0 && it < 8) { TL[16 + it] = CK(); TL[48 + it] = bw; }''')
+rep('''      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();''', '''      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      if (leader && it < 8) TL[24 + it] = CK();''')
+rep('''        mbar_arrive_remote(mapa_shared(smem_u32(&tempty[acc]), 0));''', '''        mbar_arrive_remote(mapa_shared(smem_u32(&tempty[acc]), 0));
+        if (it < 8) TL[32 + it] = CK();''')
+rep('''    if (lane == 0) tma_store_wait_all<0>();''', '''    if (lane == 0) tma_store_wait_all<0>();
+    if (leader) { TL[40] = CK(); TL[41] = GT(); TL[42] = t_end - t_begin; }''')
+(ROOT / "exp/kv_proj_tc_tl.cu").write_text(s)
+print("wrote exp/kv_proj_tc_tl.cu")

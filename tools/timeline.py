@@ -1,0 +1,56 @@
+"""Development aid: per-CTA timeline of one cfg2 K'+V' launch from the instrumented build
+(tools/instrument.py -> exp/tl.so; run with BD_LIB_PATH=exp/tl.so).  Prints medians over
+the pairs with a full tile count of: prologue stamps, each tile's MMA window (post
+tempty-wait .. last MMA issued), the epilogue window (tfull .. done), B-wait clocks.
+SM clocks relative to each CTA's entry.  Not a bench."""
+import ctypes
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np
+import torch
+
+import paper_2510_01718_b200 as bd
+from paper_2510_01718_b200 import _native
+
+L = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
+back_to_back = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+d, d_h, n = 512, 128, 16
+dev = torch.device("cuda:0")
+x = torch.randn(L, d, device=dev).half()
+ck = (torch.randn(d - d_h, n * d_h, device=dev) / 8).half()
+cv = (torch.randn(d - d_h, n * d_h, device=dev) / 8).half()
+k = torch.empty(L, n * d_h, device=dev, dtype=torch.half)
+v = torch.empty_like(k)
+specs = [(ck, d_h, n, bd.Tag.FIRST), (cv, d_h, n, bd.Tag.LAST)]
+for _ in range(10):
+    bd.fused_kv_proj_grouped(x, specs, outs=[k, v])
+torch.cuda.synchronize()
+for _ in range(back_to_back):
+    bd.fused_kv_proj_grouped(x, specs, outs=[k, v])
+torch.cuda.synchronize()
+lib = _native.load()
+buf = (ctypes.c_ulonglong * (148 * 64))()
+assert lib.bd_debug_timeline(buf) == 0
+tl = np.frombuffer(buf, dtype=np.uint64).reshape(148, 64).astype(np.int64)
+g0 = tl[:, 0].min()
+print(f"L={L} back_to_back={back_to_back}")
+print(f"CTA start spread (ns): 0 .. {tl[:, 0].max() - g0}; end (ns): "
+      f"{tl[::2, 41].min() - g0} .. {tl[::2, 41].max() - g0}")
+lead = np.arange(0, 148, 2)
+nt = tl[lead, 42]
+full = lead[nt == np.bincount(nt).argmax()]
+rel = tl[full] - tl[full, 1:2]
+med = lambda a: np.median(a, axis=0).astype(int)
+print("tiles per pair:", np.bincount(nt))
+print("prologue (prefetch, mbar-init, tmem-alloc, cluster-sync, pdl, first-TMA):",
+      med(rel[:, 2:8]))
+T = int(np.bincount(nt).argmax())
+print("mma window start:", med(rel[:, 8:8 + T]))
+print("mma issued      :", med(rel[:, 16:16 + T]))
+print("epi start (tfull):", med(rel[:, 24:24 + T]))
+print("epi end         :", med(rel[:, 32:32 + T]))
+print("b_full wait clks:", med(tl[full, 48:48 + T]))
+print("end (clk):", int(np.median(rel[:, 40])), " ns per clk ~",
+      float(np.median((tl[full, 41] - tl[full, 0]) / (tl[full, 40] - tl[full, 1]))))
