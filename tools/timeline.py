@@ -54,3 +54,12 @@ print("epi end         :", med(rel[:, 32:32 + T]))
 print("b_full wait clks:", med(tl[full, 48:48 + T]))
 print("end (clk):", int(np.median(rel[:, 40])), " ns per clk ~",
       float(np.median((tl[full, 41] - tl[full, 0]) / (tl[full, 40] - tl[full, 1]))))
+endns = tl[full, 41] - g0
+print("7-tile pair end (ns) percentiles 0/25/50/75/100:", np.percentile(endns, [0, 25, 50, 75, 100]).astype(int))
+first_mma = rel[:, 8]
+print("first MMA window start (clk) percentiles:", np.percentile(first_mma, [0, 25, 50, 75, 100]).astype(int))
+per_tile = (rel[:, 32 + T - 1] - rel[:, 32]) / (T - 1)
+print("epi-end period per tile (clk) percentiles:", np.percentile(per_tile, [0, 25, 50, 75, 100]).astype(int))
+order = np.argsort(endns)[-5:]
+print("slowest pairs (cta, end ns, first mma clk, period):",
+      [(int(full[i]), int(endns[i]), int(first_mma[i]), int(per_tile[i])) for i in order])
