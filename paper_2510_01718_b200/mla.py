@@ -60,6 +60,7 @@ class MLAConfig:
     v_head: int = 128
     rope_theta: float = 10000.0
     rms_eps: float = 1e-6
+    rope_interleaved: bool = True  # DeepSeek-V2: complex rotation of adjacent pairs
 
     @property
     def qk_head(self) -> int:
@@ -186,11 +187,19 @@ def _rms_norm(x: torch.Tensor, weight: torch.Tensor, eps: float) -> torch.Tensor
     return (y * weight.float()).to(x.dtype)
 
 
-def _rope(t: torch.Tensor, theta: float) -> torch.Tensor:
-    """Rotate-half RoPE over the last dim of [L, ..., r] at positions 0..L-1."""
+def _rope(t: torch.Tensor, theta: float, interleaved: bool = True) -> torch.Tensor:
+    """RoPE over the last dim of [L, ..., r] at positions 0..L-1, in float32.
+
+    ``interleaved``: DeepSeek-V2's form — adjacent pairs (2i, 2i+1) are one complex
+    number rotated by pos * theta^(-2i/r) (transformers ``modeling_deepseek_v2.py``
+    ``apply_rotary_emb`` [ext]); otherwise rotate-half (Llama convention)."""
     L, r = t.shape[0], t.shape[-1]
-    inv = theta ** (-torch.arange(0, r, 2, device=t.device, dtype=torch.float32) / r)
+    inv = 1.0 / (theta ** (torch.arange(0, r, 2, device=t.device, dtype=torch.int64).float() / r))
     ang = torch.arange(L, device=t.device, dtype=torch.float32)[:, None] * inv[None, :]
+    if interleaved:
+        tc = torch.view_as_complex(t.float().reshape(*t.shape[:-1], r // 2, 2).contiguous())
+        rot = torch.polar(torch.ones_like(ang), ang).view((L,) + (1,) * (t.dim() - 2) + (r // 2,))
+        return torch.view_as_real(tc * rot).flatten(-2).to(t.dtype)
     cos = torch.cat([ang.cos(), ang.cos()], -1)
     sin = torch.cat([ang.sin(), ang.sin()], -1)
     shape = (L,) + (1,) * (t.dim() - 2) + (r,)
@@ -235,7 +244,8 @@ def mla_forward(hidden: torch.Tensor, w: MLAWeights, *, causal: bool = True) -> 
     kvb = (c_kv @ w.w_kvb).view(-1, H, cfg.qk_nope + cfg.v_head)
     k_nope = kvb[..., :cfg.qk_nope].reshape(-1, H * cfg.qk_nope)
     v = kvb[..., cfg.qk_nope:].reshape(-1, H * cfg.v_head)
-    o = _mla_attend(q_nope, _rope(q_pe, cfg.rope_theta), k_nope, _rope(k_pe, cfg.rope_theta), v,
+    rope = lambda t: _rope(t, cfg.rope_theta, cfg.rope_interleaved)  # noqa: E731
+    o = _mla_attend(q_nope, rope(q_pe), k_nope, rope(k_pe), v,
                     H, cfg, causal)
     return o @ w.w_o
 
@@ -250,11 +260,103 @@ def bd_mla_forward(hidden: torch.Tensor, w: BDMLAWeights, *, causal: bool = True
     c_kv, k_pe = _latent(hidden, w.w_kva, w.kva_norm, cfg)
     k_nope, v = fused_kv_proj_grouped(c_kv, [(w.c_qk, cfg.qk_nope, H, w.qk_tag),
                                              (w.c_vo, cfg.v_head, H, w.vo_tag)])
-    o = _mla_attend(q_nope, _rope(q_pe, cfg.rope_theta), k_nope, _rope(k_pe, cfg.rope_theta), v,
+    rope = lambda t: _rope(t, cfg.rope_theta, cfg.rope_interleaved)  # noqa: E731
+    o = _mla_attend(q_nope, rope(q_pe), k_nope, rope(k_pe), v,
                     H, cfg, causal)
     out = o @ w.b_vo
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(out, group=group)
+    return out
+
+
+# --------------------------------------------------------------------------- checkpoints
+# Hugging Face DeepseekV2Attention parameter names (transformers 5.5
+# models/deepseek_v2/modeling_deepseek_v2.py:310-333 [ext]); nn.Linear stores [out, in],
+# this module uses x @ W ([in, out]).
+_HF_DENSE = ("q_proj.weight", "kv_a_proj_with_mqa.weight", "kv_a_layernorm.weight",
+             "kv_b_proj.weight", "o_proj.weight")
+
+
+def mla_config_from_hf(hf_config) -> MLAConfig:
+    """MLAConfig from a transformers DeepseekV2Config (q-LoRA-free attention only)."""
+    if getattr(hf_config, "q_lora_rank", None) is not None:
+        raise ShapeError("q_lora_rank set: only the q_proj (no q-LoRA) attention is supported")
+    rope = getattr(hf_config, "rope_parameters", None) or {}
+    return MLAConfig(hidden=hf_config.hidden_size, n_heads=hf_config.num_attention_heads,
+                     kv_lora_rank=hf_config.kv_lora_rank, qk_nope=hf_config.qk_nope_head_dim,
+                     qk_rope=hf_config.qk_rope_head_dim, v_head=hf_config.v_head_dim,
+                     rope_theta=float(rope.get("rope_theta", getattr(hf_config, "rope_theta", 10000.0))),
+                     rms_eps=float(hf_config.rms_norm_eps), rope_interleaved=True)
+
+
+def mla_from_hf(state: dict, cfg: MLAConfig, prefix: str = "") -> MLAWeights:
+    """Dense MLAWeights from a DeepseekV2Attention state dict (keys under ``prefix``).
+    kv_b_proj's rows are per head [k_nope | v] — already this module's column order."""
+    missing = [k for k in _HF_DENSE if prefix + k not in state]
+    if missing:
+        raise ShapeError(f"state dict lacks {missing} under prefix {prefix!r}")
+    g = lambda k: state[prefix + k].detach()  # noqa: E731
+    H = cfg.n_heads
+    w = MLAWeights(cfg=cfg, w_q=g("q_proj.weight").T.contiguous(),
+                   w_kva=g("kv_a_proj_with_mqa.weight").T.contiguous(),
+                   kva_norm=g("kv_a_layernorm.weight").contiguous(),
+                   w_kvb=g("kv_b_proj.weight").T.contiguous(),
+                   w_o=g("o_proj.weight").T.contiguous())
+    want = {"w_q": (cfg.hidden, H * cfg.qk_head), "w_kva": (cfg.hidden, cfg.kv_lora_rank + cfg.qk_rope),
+            "kva_norm": (cfg.kv_lora_rank,), "w_kvb": (cfg.kv_lora_rank, H * (cfg.qk_nope + cfg.v_head)),
+            "w_o": (H * cfg.v_head, cfg.hidden)}
+    for k, shp in want.items():
+        if tuple(getattr(w, k).shape) != shp:
+            raise ShapeError(f"{k}: shape {tuple(getattr(w, k).shape)}, expected {shp}")
+    return w
+
+
+def bd_mla_state_dict(w: BDMLAWeights, prefix: str = "") -> dict:
+    """The rewritten checkpoint of one attention layer: q_proj carries B_qk in each head's
+    nope columns, kv_b_proj is replaced by the two coefficient matrices (reference layout)
+    and their tags, o_proj carries B_vo.  [out, in] like the original."""
+    tag = lambda t: torch.tensor(0 if t is Tag.FIRST else 1, dtype=torch.int8)  # noqa: E731
+    return {prefix + "q_proj.weight": w.w_q.T.contiguous(),
+            prefix + "kv_a_proj_with_mqa.weight": w.w_kva.T.contiguous(),
+            prefix + "kv_a_layernorm.weight": w.kva_norm.contiguous(),
+            prefix + "kv_b_proj.c_qk": w.c_qk.contiguous(),
+            prefix + "kv_b_proj.c_vo": w.c_vo.contiguous(),
+            prefix + "kv_b_proj.qk_tag": tag(w.qk_tag),
+            prefix + "kv_b_proj.vo_tag": tag(w.vo_tag),
+            prefix + "o_proj.weight": w.b_vo.T.contiguous()}
+
+
+def bd_mla_from_state_dict(state: dict, cfg: MLAConfig, prefix: str = "") -> BDMLAWeights:
+    """Inverse of ``bd_mla_state_dict`` (candidate residuals are not stored: NaN)."""
+    g = lambda k: state[prefix + k].detach()  # noqa: E731
+    tag = lambda k: Tag.FIRST if int(g(k)) == 0 else Tag.LAST  # noqa: E731
+    c_qk, c_vo = g("kv_b_proj.c_qk").contiguous(), g("kv_b_proj.c_vo").contiguous()
+    H = c_qk.shape[1] // cfg.qk_nope
+    if c_qk.shape != (cfg.kv_lora_rank - cfg.qk_nope, H * cfg.qk_nope) or \
+            c_vo.shape != (cfg.kv_lora_rank - cfg.v_head, H * cfg.v_head):
+        raise ShapeError(f"coefficient shapes {tuple(c_qk.shape)}, {tuple(c_vo.shape)} do not fit {cfg}")
+    nan = (float("nan"), float("nan"))
+    return BDMLAWeights(cfg=cfg, w_q=g("q_proj.weight").T.contiguous(),
+                        w_kva=g("kv_a_proj_with_mqa.weight").T.contiguous(),
+                        kva_norm=g("kv_a_layernorm.weight").contiguous(), c_qk=c_qk, c_vo=c_vo,
+                        b_vo=g("o_proj.weight").T.contiguous(), qk_tag=tag("kv_b_proj.qk_tag"),
+                        vo_tag=tag("kv_b_proj.vo_tag"), qk_candidate_residuals=nan,
+                        vo_candidate_residuals=nan, n_heads=H)
+
+
+def rewrite_hf_checkpoint(state: dict, cfg: MLAConfig, *, dtype: torch.dtype | None = None,
+                          force_first: bool = False) -> dict:
+    """Rewrite every DeepseekV2Attention in a model state dict (keys ``...self_attn.``)
+    to its BD form (offline, float64 prep, cast back to ``dtype`` or the stored dtype);
+    all other entries pass through unchanged."""
+    prefixes = sorted({k[:-len("kv_b_proj.weight")] for k in state if k.endswith("kv_b_proj.weight")})
+    out = {k: v for k, v in state.items()
+           if not any(k.startswith(p) and k[len(p):] in _HF_DENSE for p in prefixes)}
+    for p in prefixes:
+        dense = mla_from_hf(state, cfg, p)
+        dt = dtype or dense.w_kvb.dtype
+        bdw = mla_prepare(dense.to(dtype=torch.float64), force_first=force_first).to(dtype=dt)
+        out.update(bd_mla_state_dict(bdw, p))
     return out
 
 

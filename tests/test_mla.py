@@ -101,3 +101,77 @@ def test_head_sharded_mla_partials_sum_to_the_full_block(cuda):
     for world in (2, 4):
         parts = [M.bd_mla_forward(hid, M.shard_bd_mla(p, world, r)) for r in range(world)]
         assert bd.max_relative_error(sum(parts), full) <= 1e-12
+
+
+def _hf_attention(seed=11):
+    """A small transformers DeepseekV2Attention (q-LoRA-free, like DSV2-Lite) with every
+    parameter random (including the kv_a RMSNorm weight), float64, SDPA causal."""
+    pytest.importorskip("transformers")
+    from transformers.models.deepseek_v2 import modeling_deepseek_v2 as HF
+    from transformers.models.deepseek_v2.configuration_deepseek_v2 import DeepseekV2Config
+    hcfg = DeepseekV2Config(hidden_size=96, num_attention_heads=4, num_key_value_heads=4,
+                            kv_lora_rank=48, q_lora_rank=None, qk_nope_head_dim=16,
+                            qk_rope_head_dim=8, v_head_dim=16, max_position_embeddings=256)
+    hcfg._attn_implementation = "sdpa"
+    torch.manual_seed(seed)
+    att = HF.DeepseekV2Attention(hcfg, 0).double()
+    with torch.no_grad():
+        for name, prm in att.named_parameters():
+            prm.copy_(torch.randn_like(prm) / (prm.shape[-1] ** 0.5 if prm.dim() == 2 else 1.0)
+                      + (1.0 if prm.dim() == 1 else 0.0))
+    rot = HF.DeepseekV2RotaryEmbedding(hcfg)
+    return hcfg, att, rot
+
+
+def _hf_forward(att, rot, hid):
+    pe = rot(hid[None], torch.arange(hid.shape[0])[None])
+    with torch.no_grad():
+        return att(hid[None], attention_mask=None, position_embeddings=pe)[0][0]
+
+
+def test_hf_deepseek_v2_attention_equals_mla_forward():
+    """The checkpoint importer and the block forward against transformers' own
+    DeepseekV2Attention (same weights, float64 except the float32 RoPE / RMSNorm both
+    implementations use)."""
+    hcfg, att, rot = _hf_attention()
+    cfg = M.mla_config_from_hf(hcfg)
+    assert cfg == M.MLAConfig(hidden=96, n_heads=4, kv_lora_rank=48, qk_nope=16, qk_rope=8,
+                              v_head=16, rope_interleaved=True)
+    hid = torch.randn(37, 96, dtype=torch.float64, generator=torch.Generator().manual_seed(2))
+    ref = _hf_forward(att, rot, hid)
+    got = M.mla_forward(hid, M.mla_from_hf(att.state_dict(), cfg))
+    assert bd.max_relative_error(got, ref) <= 1e-6  # measured 3.9e-8 (rotate-half RoPE: 0.29)
+
+
+def test_rewrite_hf_checkpoint_replaces_attention_and_round_trips():
+    hcfg, att, rot = _hf_attention(12)
+    cfg = M.mla_config_from_hf(hcfg)
+    sd = {f"model.layers.0.self_attn.{k}": v for k, v in att.state_dict().items()}
+    sd["model.layers.0.mlp.up_proj.weight"] = torch.randn(8, 96, dtype=torch.float64)
+    new = M.rewrite_hf_checkpoint(sd, cfg)
+    pre = "model.layers.0.self_attn."
+    assert pre + "kv_b_proj.weight" not in new
+    assert torch.equal(new["model.layers.0.mlp.up_proj.weight"], sd["model.layers.0.mlp.up_proj.weight"])
+    assert new[pre + "kv_b_proj.c_qk"].shape == (48 - 16, 4 * 16)
+    # 25 % fewer kv_b weights at d_h = r / 4 (here 2 x 32 x 64 vs 48 x 128)
+    n_new = new[pre + "kv_b_proj.c_qk"].numel() + new[pre + "kv_b_proj.c_vo"].numel()
+    assert n_new == 2 * 32 * 64 and sd[pre + "kv_b_proj.weight"].numel() == 48 * 128
+    back = M.bd_mla_from_state_dict(new, cfg, pre)
+    want = M.mla_prepare(M.mla_from_hf(att.state_dict(), cfg))
+    for k in ("w_q", "w_kva", "kva_norm", "c_qk", "c_vo", "b_vo"):
+        assert torch.equal(getattr(back, k), getattr(want, k)), k
+    assert (back.qk_tag, back.vo_tag, back.n_heads) == (want.qk_tag, want.vo_tag, 4)
+
+
+@pytest.mark.gpu
+def test_bd_mla_on_rewritten_hf_checkpoint_matches_hf_attention(cuda):
+    """End to end: transformers DeepseekV2Attention → rewritten BD checkpoint → the BD
+    block on the GPU (float64: exact kernel) reproduces the HF module's output."""
+    hcfg, att, rot = _hf_attention(13)
+    cfg = M.mla_config_from_hf(hcfg)
+    new = M.rewrite_hf_checkpoint(att.state_dict(), cfg)
+    w = M.bd_mla_from_state_dict(new, cfg).to(cuda)
+    hid = torch.randn(45, 96, dtype=torch.float64, generator=torch.Generator().manual_seed(3))
+    ref = _hf_forward(att, rot, hid)
+    got = M.bd_mla_forward(hid.to(cuda), w).cpu()
+    assert bd.max_relative_error(got, ref) <= 1e-6
