@@ -44,12 +44,10 @@ rep('''  tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;''', '''  tc_fence_after();
   if (threadIdx.x == 0) TL[5] = CK();
   const uint32_t tmem_base = *tmem_slot;''')
-rep('''  griddep_wait();
-  griddep_launch_dependents();
-''', '''  griddep_wait();
-  griddep_launch_dependents();
-  if (threadIdx.x == 0) TL[6] = CK();
-''')
+rep('''      griddep_wait();
+      for (int t = t_begin; t < t_end; ++t) {''', '''      griddep_wait();
+      if (lane == 0) TL[6] = CK();
+      for (int t = t_begin; t < t_end; ++t) {''')
 rep('''            const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), 0);''', '''            const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), 0);
             if (b_iter == 0) TL[7] = CK();''')
 rep('''        mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -72,5 +70,13 @@ rep('''        mbar_arrive_remote(mapa_shared(smem_u32(&tempty[acc]), 0));''', '
         if (it < 8) TL[32 + it] = CK();''')
 rep('''    if (lane == 0) tma_store_wait_all<0>();''', '''    if (lane == 0) tma_store_wait_all<0>();
     if (leader) { TL[40] = CK(); TL[41] = GT(); TL[42] = t_end - t_begin; }''')
+rep('''        const bool reload_a = P.num_kb > A_SLOTS || key != prev_key;
+        prev_key = key;
+        const int my_m0''', '''        const bool reload_a = P.num_kb > A_SLOTS || key != prev_key;
+        if (t == t_begin && lane == 0) TL[43] = CK() + (reload_a ? 0 : 1);
+        prev_key = key;
+        const int my_m0''')
+rep('''            mbar_wait(&a_empty[s], ((a_iter / A_SLOTS) & 1u) ^ 1u);''', '''            mbar_wait(&a_empty[s], ((a_iter / A_SLOTS) & 1u) ^ 1u);
+            if (a_iter == 0 && lane == 0) TL[44] = CK();''')
 (ROOT / "exp/kv_proj_tc_tl.cu").write_text(s)
 print("wrote exp/kv_proj_tc_tl.cu")

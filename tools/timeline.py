@@ -47,6 +47,7 @@ print("tiles per pair:", np.bincount(nt))
 print("prologue (prefetch, mbar-init, tmem-alloc, cluster-sync, pdl, first-TMA):",
       med(rel[:, 2:8]))
 T = int(np.bincount(nt).argmax())
+print("producer: first decode done, first a_empty passed:", med(rel[:, 43:45]))
 print("mma window start:", med(rel[:, 8:8 + T]))
 print("mma issued      :", med(rel[:, 16:16 + T]))
 print("epi start (tfull):", med(rel[:, 24:24 + T]))
