@@ -44,6 +44,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 
@@ -100,7 +101,9 @@ struct TcParams {
   TcProblem p[BD_MAX_GROUP];
   // fused all-gather: per problem, the head-major 3-D map {d_h, L, world * n_heads} of
   // every rank's gathered buffer (peer memory over NVLink); world == 0 otherwise
-  CUtensorMap map_peer[BD_MAX_GROUP][BD_MAX_PEERS];
+  // [count][world] in device memory (kept out of the kernel parameters: 4 KB more of
+  // them costs ~2 us of host time per launch); null when world == 0
+  const CUtensorMap* peer_maps;
   int32_t world;
   int32_t head0[BD_MAX_GROUP];
   int32_t count;
@@ -458,6 +461,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       griddep_wait();
       if (fast0) issue_rep(t_begin);
     }
+    if (prm.world > 0 && lane == 0) {
+      // peer tensor maps were copied to global memory before the launch: order those
+      // generic-proxy writes before the TMA unit's descriptor reads
+      for (int i = 0; i < prm.count * prm.world; ++i)
+        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(
+                         reinterpret_cast<uint64_t>(prm.peer_maps + i))
+                     : "memory");
+    }
     uint32_t chk = 0u;  // NaN-propagating packed max |out| (16-bit) for the non-finite check
     uint32_t rep_loads = 0;
     int cur_key = -1;   // row-block whose rep values are in repv (-1: none)
@@ -572,7 +583,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int r = 0; r < prm.world; ++r)
                 asm volatile(
                     "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                        reinterpret_cast<uint64_t>(&prm.map_peer[pi][r])),
+                        reinterpret_cast<uint64_t>(prm.peer_maps + pi * prm.world + r)),
                     "r"(stg0), "r"(bcol % P.out_d_h), "r"(brow),
                     "r"(prm.head0[pi] + bcol / P.out_d_h)
                     : "memory");
@@ -705,13 +716,106 @@ bool encode_3d(CUtensorMap* map, const void* base, bool bf16, uint64_t cols, uin
 
 }  // namespace tc
 
+namespace {
+
+// Launch-parameter cache.  Encoding the tensor maps (four per problem, plus one per peer)
+// is most of the library's host time per call (~10 us for cfg2); a serving loop calls
+// with the same buffers over and over, so the encoded TcParams are kept per problem
+// signature.  Tensor maps are pure host-side encodings of (pointer, shape, strides,
+// box): an identical signature yields identical maps.
+struct ParamKey {
+  int32_t count;
+  int32_t bf16;
+  Problem p[BD_MAX_GROUP];
+};
+struct ParamEntry {
+  bool valid;
+  ParamKey key;
+  tc::TcParams prm;
+};
+constexpr int kParamCacheSize = 8;
+std::mutex g_param_mu;
+ParamEntry g_param_cache[kParamCacheSize];
+int g_param_next = 0;
+
+ParamKey make_key(const Problem* probs, int count, bool bf16) {
+  ParamKey k;
+  memset(&k, 0, sizeof(k));  // padding included: keys compare with memcmp
+  k.count = count;
+  k.bf16 = bf16 ? 1 : 0;
+  for (int i = 0; i < count; ++i) {
+    const Problem& q = probs[i];
+    Problem& d = k.p[i];
+    d.x = q.x;
+    d.c = q.c;
+    d.out = q.out;
+    d.ldx = q.ldx;
+    d.ldc = q.ldc;
+    d.ldo = q.ldo;
+    d.L = q.L;
+    d.K = q.K;
+    d.N = q.N;
+    d.d_h = q.d_h;
+    d.mul_base = q.mul_base;
+    d.rep_base = q.rep_base;
+    d.out_layout = q.out_layout;
+    d.world = q.world;
+    d.head0 = q.head0;
+    for (int r = 0; r < q.world && r < BD_MAX_PEERS; ++r) d.peers[r] = q.peers[r];
+  }
+  return k;
+}
+
+int build_params(const Problem* probs, int count, bool bf16, tc::TcParams& prm,
+                 cudaStream_t stream);
+int launch_params(const tc::TcParams& prm, int total, bool bf16, bool check,
+                  cudaStream_t stream);
+
+}  // namespace
+
 int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_t stream) {
   using namespace tc;
-  constexpr int cg = CG;
   const bool bf16 = dtype == BD_BF16;
-  TcParams prm{};
-  prm.count = count;
+  TcParams prm;
+  {
+    const ParamKey key = make_key(probs, count, bf16);
+    std::lock_guard<std::mutex> lock(g_param_mu);
+    int hit = -1;
+    for (int i = 0; i < kParamCacheSize; ++i)
+      if (g_param_cache[i].valid && memcmp(&g_param_cache[i].key, &key, sizeof(key)) == 0) {
+        hit = i;
+        break;
+      }
+    if (hit >= 0) {
+      prm = g_param_cache[hit].prm;
+    } else {
+      const int st = build_params(probs, count, bf16, prm, stream);
+      if (st != BD_OK) return st;
+      ParamEntry& e = g_param_cache[g_param_next];
+      g_param_next = (g_param_next + 1) % kParamCacheSize;
+      // an evicted all-gather entry owns its device copy of the peer maps (cudaFree waits
+      // for any kernel still reading them)
+      if (e.valid && e.prm.peer_maps) cudaFree(const_cast<CUtensorMap*>(e.prm.peer_maps));
+      e.key = key;
+      e.prm = prm;
+      e.valid = true;
+    }
+  }
   prm.flag = flag;
+  const int total = prm.total_tiles;
+  if (total == 0) return BD_OK;
+  return launch_params(prm, total, bf16, flag != nullptr, stream);
+}
+
+namespace {
+
+int build_params(const Problem* probs, int count, bool bf16, tc::TcParams& prm,
+                 cudaStream_t stream) {
+  using namespace tc;
+  constexpr int cg = CG;
+  prm = TcParams{};
+  CUtensorMap peer_host[BD_MAX_GROUP * BD_MAX_PEERS];
+  prm.count = count;
   int total = 0;
   for (int i = 0; i < count; ++i) {
     const Problem& q = probs[i];
@@ -742,7 +846,7 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
       prm.world = q.world;
       prm.head0[i] = q.head0;
       for (int r = 0; r < q.world; ++r)
-        if (!encode_3d(&prm.map_peer[i][r], q.peers[r], bf16, q.d_h, q.L,
+        if (!encode_3d(&peer_host[i * q.world + r], q.peers[r], bf16, q.d_h, q.L,
                        static_cast<uint64_t>(q.world) * (N / q.d_h), q.ldo, q.L * q.ldo, 64, 32,
                        &err)) {
           set_error(err);
@@ -764,10 +868,33 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
     total += P.tiles_n * static_cast<int32_t>((q.L + BM * cg - 1) / (BM * cg));
   }
   prm.total_tiles = total;
-  if (total == 0) return BD_OK;
+  if (prm.world > 0) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &cap);
+    if (cap != cudaStreamCaptureStatusNone) {
+      set_error("fused all-gather: the first call with a given set of buffers must run "
+                "outside stream capture (its peer tensor maps are uploaded then)");
+      return BD_ERR_ARG;
+    }
+    const size_t bytes = sizeof(CUtensorMap) * static_cast<size_t>(count) * prm.world;
+    void* dev = nullptr;
+    cudaError_t e = cudaMalloc(&dev, bytes);
+    if (e == cudaSuccess) e = cudaMemcpy(dev, peer_host, bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      if (dev) cudaFree(dev);
+      set_error(std::string("fused all-gather tensor maps: ") + cudaGetErrorString(e));
+      return BD_ERR_CUDA;
+    }
+    prm.peer_maps = static_cast<const CUtensorMap*>(dev);
+  }
+  return BD_OK;
+}
 
+int launch_params(const tc::TcParams& prm, int total, bool bf16, bool check,
+                  cudaStream_t stream) {
+  using namespace tc;
+  constexpr int cg = CG;
   using KernFn = void (*)(TcParams);
-  const bool check = flag != nullptr;
   KernFn kern = bf16 ? (check ? kv_proj_tc_kernel<true, true> : kv_proj_tc_kernel<true, false>)
                      : (check ? kv_proj_tc_kernel<false, true> : kv_proj_tc_kernel<false, false>);
   const size_t smem = SMEM_BYTES;
@@ -810,5 +937,7 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
   }
   return BD_OK;
 }
+
+}  // namespace
 
 }  // namespace bdk

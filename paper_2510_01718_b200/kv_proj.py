@@ -109,6 +109,23 @@ def _problem(x, c, out, d_h, n_heads, tag) -> N.KvProblem:
                        ldo, L, d, d_h, n_heads, mul_base, rep_base)
 
 
+_raw_stream_fn = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def _on_device(dev: torch.device, fn, *args):
+    """Call a C-ABI entry point with the device's current stream appended, making the
+    device current only when it is not already (the context manager costs microseconds
+    per call on an eager serving path)."""
+    cur = torch.cuda.current_device()
+    idx = cur if dev.index is None else dev.index
+    if idx == cur:
+        stream = (_raw_stream_fn(idx) if _raw_stream_fn is not None
+                  else torch.cuda.current_stream(idx).cuda_stream)
+        return fn(*args, stream)
+    with torch.cuda.device(idx):
+        return fn(*args, torch.cuda.current_stream(idx).cuda_stream)
+
+
 def _finish(flag: torch.Tensor | None) -> None:
     if flag is not None and int(flag.item()) != 0:
         raise ValueError("operation produced non-finite values")
@@ -132,12 +149,9 @@ def fused_kv_proj(x: torch.Tensor, c: torch.Tensor, d_h: int, n_heads: int,
     out = _out_tensor(x, d_h, n_heads, out_layout, out)
     flag = torch.zeros(1, dtype=torch.int32, device=x.device) if check_finite else None
     prob = _problem(x, c, out, d_h, n_heads, tag)
-    stream = torch.cuda.current_stream(x.device).cuda_stream
-    with torch.cuda.device(x.device):
-        st = N.load().bd_kv_proj_grouped_ex(ctypes.byref(prob), 1, _DTYPES[x.dtype],
-                                            _MODES[mode], _LAYOUTS[out_layout],
-                                            flag.data_ptr() if flag is not None else None,
-                                            stream)
+    st = _on_device(x.device, N.load().bd_kv_proj_grouped_ex, ctypes.byref(prob), 1,
+                    _DTYPES[x.dtype], _MODES[mode], _LAYOUTS[out_layout],
+                    flag.data_ptr() if flag is not None else None)
     N.check(st, "bd_kv_proj")
     _finish(flag)
     return out
@@ -168,12 +182,9 @@ def fused_kv_proj_grouped(x: torch.Tensor,
     own_flag = flag is None and check_finite
     if own_flag:
         flag = torch.zeros(1, dtype=torch.int32, device=x.device)
-    stream = torch.cuda.current_stream(x.device).cuda_stream
-    with torch.cuda.device(x.device):
-        st = N.load().bd_kv_proj_grouped_ex(probs, len(specs), _DTYPES[x.dtype], _MODES[mode],
-                                            _LAYOUTS[out_layout],
-                                            flag.data_ptr() if flag is not None else None,
-                                            stream)
+    st = _on_device(x.device, N.load().bd_kv_proj_grouped_ex, probs, len(specs),
+                    _DTYPES[x.dtype], _MODES[mode], _LAYOUTS[out_layout],
+                    flag.data_ptr() if flag is not None else None)
     N.check(st, "bd_kv_proj_grouped")
     if own_flag:
         _finish(flag)

@@ -23,7 +23,7 @@ import torch
 from . import _native as N
 from .decompose import Axis, BDFactors, Tag, bd_decompose, ordered_matmul
 from .errors import NativeLibraryError, PrecisionError, ShapeError
-from .kv_proj import _DTYPES, _MODES, _rowmajor
+from .kv_proj import _DTYPES, _MODES, _on_device, _rowmajor
 
 
 @dataclass(frozen=True)
@@ -143,13 +143,11 @@ def bd_linear_forward(x: torch.Tensor, layer: BDLinearLayer, *, out: torch.Tenso
         raise ShapeError("out must be a row-major (L, d_out) tensor of x's dtype")
     flag = torch.zeros(1, dtype=torch.int32, device=x.device) if check_finite else None
     tag = N.BD_TAG_FIRST if layer.tag is Tag.FIRST else N.BD_TAG_LAST
-    stream = torch.cuda.current_stream(x.device).cuda_stream
-    with torch.cuda.device(x.device):
-        st = N.load().bd_linear_forward(
-            x.data_ptr(), x.stride(0), basis.data_ptr(), basis.stride(0), coeff.data_ptr(),
-            coeff.stride(0), out.data_ptr(), out.stride(0), L, layer.d_in, layer.rank,
-            layer.d_out, tag, _DTYPES[x.dtype], _MODES[mode],
-            flag.data_ptr() if flag is not None else None, stream)
+    st = _on_device(x.device, N.load().bd_linear_forward,
+                    x.data_ptr(), x.stride(0), basis.data_ptr(), basis.stride(0),
+                    coeff.data_ptr(), coeff.stride(0), out.data_ptr(), out.stride(0), L,
+                    layer.d_in, layer.rank, layer.d_out, tag, _DTYPES[x.dtype], _MODES[mode],
+                    flag.data_ptr() if flag is not None else None)
     N.check(st, "bd_linear_forward")
     if flag is not None and int(flag.item()) != 0:
         raise ValueError("operation produced non-finite values")
@@ -167,10 +165,8 @@ def matmul(a: torch.Tensor, b: torch.Tensor, *, mode: str = "auto") -> torch.Ten
         raise NativeLibraryError("matmul needs CUDA tensors (no CPU fallback)")
     a, b = _rowmajor(a), _rowmajor(b)
     out = torch.empty((a.shape[0], b.shape[1]), dtype=a.dtype, device=a.device)
-    stream = torch.cuda.current_stream(a.device).cuda_stream
-    with torch.cuda.device(a.device):
-        st = N.load().bd_matmul(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0),
-                                out.data_ptr(), out.stride(0), a.shape[0], a.shape[1],
-                                b.shape[1], _DTYPES[a.dtype], _MODES[mode], None, stream)
+    st = _on_device(a.device, N.load().bd_matmul, a.data_ptr(), a.stride(0), b.data_ptr(),
+                    b.stride(0), out.data_ptr(), out.stride(0), a.shape[0], a.shape[1],
+                    b.shape[1], _DTYPES[a.dtype], _MODES[mode], None)
     N.check(st, "bd_matmul")
     return out

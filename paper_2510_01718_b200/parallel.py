@@ -37,7 +37,8 @@ import ctypes
 from . import _native as N
 from .attention import BDAWeights, _attend, _proj
 from .decompose import Tag
-from .kv_proj import _DTYPES, _MODES, _check, _problem, _rowmajor, fused_kv_proj_grouped
+from .kv_proj import (_DTYPES, _MODES, _check, _on_device, _problem, _rowmajor,
+                      fused_kv_proj_grouped)
 
 
 def head_range(n_heads: int, world: int, rank: int) -> tuple[int, int]:
@@ -147,10 +148,8 @@ def fused_allgather_kv_proj(x: torch.Tensor,
                                  f"{x.dtype} tensor")
             ptrs[i * world + r] = g.data_ptr()
         probs[i] = _problem(x, c, gathered[i][rank][rank * n:(rank + 1) * n], d_h, n, tag)
-    stream = torch.cuda.current_stream(x.device).cuda_stream
-    with torch.cuda.device(x.device):
-        st = N.load().bd_kv_proj_grouped_allgather(probs, len(specs), _DTYPES[x.dtype],
-                                                   _MODES[mode], world, rank, ptrs, None, stream)
+    st = _on_device(x.device, N.load().bd_kv_proj_grouped_allgather, probs, len(specs),
+                    _DTYPES[x.dtype], _MODES[mode], world, rank, ptrs, None)
     N.check(st, "bd_kv_proj_grouped_allgather")
 
 

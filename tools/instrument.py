@@ -5,7 +5,9 @@ tools/timeline.py.  Build:  cd paper_2510_01718_b200/csrc && nvcc <build flags> 
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-s = (ROOT / "paper_2510_01718_b200/csrc/kv_proj_tc.cu").read_text()
+import sys
+SRC = sys.argv[1] if len(sys.argv) > 1 else "paper_2510_01718_b200/csrc/kv_proj_tc.cu"
+s = (ROOT / SRC).read_text()
 
 
 def rep(a, b):
@@ -48,7 +50,10 @@ rep('''      griddep_wait();
       for (int t = t_begin; t < t_end; ++t) {''', '''      griddep_wait();
       if (lane == 0) TL[6] = CK();
       for (int t = t_begin; t < t_end; ++t) {''')
-rep('''            const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), 0);''', '''            const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), 0);
+for lead in ("0", "lead"):
+    a = f'''            const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), {lead});'''
+    if s.count(a) == 1:
+        rep(a, a + '''
             if (b_iter == 0) TL[7] = CK();''')
 rep('''        mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();''', '''        mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -58,15 +63,20 @@ rep('''        mbar_wait(&tempty[acc], acc_phase ^ 1);
 rep('''          mbar_wait(&b_full[bs], (b_iter / B_STAGES) & 1u);''', '''          const unsigned long long w0 = CK();
           mbar_wait(&b_full[bs], (b_iter / B_STAGES) & 1u);
           bw += CK() - w0;''')
-rep('''        if (elect_one()) tc_commit_pair(&tfull[acc], 0x3);
-        __syncwarp();''', '''        if (elect_one()) tc_commit_pair(&tfull[acc], 0x3);
-        __syncwarp();
+for m in ("0x3", "pmask"):
+    a = f'''        if (elect_one()) tc_commit_pair(&tfull[acc], {m});
+        __syncwarp();'''
+    if s.count(a) == 1:
+        rep(a, a + '''
         if (lane == 0 && it < 8) { TL[16 + it] = CK(); TL[48 + it] = bw; }''')
 rep('''      mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();''', '''      mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (leader && it < 8) TL[24 + it] = CK();''')
-rep('''        mbar_arrive_remote(mapa_shared(smem_u32(&tempty[acc]), 0));''', '''        mbar_arrive_remote(mapa_shared(smem_u32(&tempty[acc]), 0));
+for lead in ("0", "lead"):
+    a = f'''        mbar_arrive_remote(mapa_shared(smem_u32(&tempty[acc]), {lead}));'''
+    if s.count(a) == 1:
+        rep(a, a + '''
         if (it < 8) TL[32 + it] = CK();''')
 rep('''    if (lane == 0) tma_store_wait_all<0>();''', '''    if (lane == 0) tma_store_wait_all<0>();
     if (leader) { TL[40] = CK(); TL[41] = GT(); TL[42] = t_end - t_begin; }''')

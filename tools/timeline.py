@@ -16,19 +16,21 @@ from paper_2510_01718_b200 import _native
 
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 back_to_back = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-d, d_h, n = 512, 128, 16
+n = int(sys.argv[3]) if len(sys.argv) > 3 else 16
+single = len(sys.argv) > 4 and sys.argv[4] == "single"
+d, d_h = 512, 128
 dev = torch.device("cuda:0")
 x = torch.randn(L, d, device=dev).half()
 ck = (torch.randn(d - d_h, n * d_h, device=dev) / 8).half()
 cv = (torch.randn(d - d_h, n * d_h, device=dev) / 8).half()
 k = torch.empty(L, n * d_h, device=dev, dtype=torch.half)
 v = torch.empty_like(k)
-specs = [(ck, d_h, n, bd.Tag.FIRST), (cv, d_h, n, bd.Tag.LAST)]
+specs = [(ck, d_h, n, bd.Tag.FIRST)] + ([] if single else [(cv, d_h, n, bd.Tag.LAST)])
 for _ in range(10):
-    bd.fused_kv_proj_grouped(x, specs, outs=[k, v])
+    bd.fused_kv_proj_grouped(x, specs, outs=[k, v][:len(specs)])
 torch.cuda.synchronize()
 for _ in range(back_to_back):
-    bd.fused_kv_proj_grouped(x, specs, outs=[k, v])
+    bd.fused_kv_proj_grouped(x, specs, outs=[k, v][:len(specs)])
 torch.cuda.synchronize()
 lib = _native.load()
 buf = (ctypes.c_ulonglong * (148 * 64))()
