@@ -95,6 +95,8 @@ struct TcProblem {
   int32_t rep_fast;     // d_h in {64, 128}: rep tile staged in smem by TMA
   int32_t head_major;   // output layout [n_heads][L][d_h]
   int32_t out_d_h;      // head width of the head-major output
+  void* out;            // output base and row stride (the small-L kernel stores directly)
+  int64_t ldo;
 };
 
 struct TcParams {
@@ -108,6 +110,7 @@ struct TcParams {
   int32_t head0[BD_MAX_GROUP];
   int32_t count;
   int32_t total_tiles;  // tiles of (BM * CG) rows x BN columns
+  int32_t a_kb_bytes;   // small-L kernel: bytes of one A k-block (rows rounded to 8 x 128 B)
   int* flag;            // non-finite flag (kCheck instantiation only)
 };
 
@@ -645,6 +648,166 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------------
+// Small-L ("decode") kernel: L <= 128 tokens, K <= 384.  The persistent pair kernel
+// spends a full 256-row tile, its prologue and a 256-column epilogue per output block —
+// ~8 us whatever L is.  Here each CTA owns one BNS-column block of one problem for all
+// (<= 128) rows: its whole A (x rows, L x K) and B (K x BNS) slices are loaded at once
+// (one barrier per 64-deep k-block so the MMAs start on the first), one M=128 x N=BNS
+// accumulator in TMEM (cta_group::1), and four epilogue warps add the repeated slice
+// (global loads, L2-resident), round and store straight to global memory.  The work is
+// streaming C once across ~128 CTAs; the same FP32 accumulation + FHADD + rounding as
+// the main kernel.
+constexpr int SM_THREADS = 64 + 128;  // producer, MMA, 4 epilogue warps
+constexpr int SM_MAX_KB = 6;          // K <= 384
+inline size_t small_smem_bytes(int bns, int a_kb_bytes) {
+  return 1024 + SM_MAX_KB * (a_kb_bytes + (bns / 64) * B_PANEL) + 128;
+}
+
+template <bool kBF16, bool kCheck, int BNS>
+__global__ void __launch_bounds__(SM_THREADS, 1)
+    kv_proj_small_kernel(const __grid_constant__ TcParams prm) {
+  constexpr int PANELS = BNS / 64;
+  constexpr uint32_t BS_BYTES = PANELS * B_PANEL;  // one k-block of this CTA's B
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // A k-blocks hold only the L (rounded up to 8) rows the box loads; the MMA still reads
+  // 128 rows, and the rows past L land in accumulator lanes that are never stored
+  const uint32_t a_kb = static_cast<uint32_t>(prm.a_kb_bytes);
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + SM_MAX_KB * a_kb;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + SM_MAX_KB * BS_BYTES);
+  uint64_t* done = full + SM_MAX_KB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+
+  int pi, m0, n0;
+  {
+    // block -> (problem, column block); tiles_n counts BNS-wide blocks here
+    const int t = static_cast<int>(blockIdx.x);
+    pi = 0;
+    while (pi + 1 < prm.count && t >= prm.p[pi + 1].tile_start) ++pi;
+    n0 = (t - prm.p[pi].tile_start) * BNS;
+    m0 = 0;
+  }
+  const TcProblem& P = prm.p[pi];
+  if (warp == 0 && lane == 0) {
+    for (int kb = 0; kb < SM_MAX_KB; ++kb) mbar_init(&full[kb], 1);
+    mbar_init(done, 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&P.map_a);
+    tma_prefetch_desc(&P.map_b);
+  }
+  if (warp == 1) {
+    tmem_alloc<1>(tmem_slot, BNS);
+    tmem_relinquish<1>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_launch_dependents();
+
+  if (warp == 0) {
+    // ---- producer: every k-block of A and B at once (nothing to recycle)
+    griddep_wait();
+    if (elect_one()) {
+      const uint64_t pol = policy_evict_last();  // C is shared by the row... and re-read
+      for (int kb = 0; kb < P.num_kb; ++kb) {
+        mbar_arrive_expect_tx(&full[kb], a_kb + BS_BYTES);
+        tma_load_2d(sA + kb * a_kb, &P.map_a, kb * BK, m0, &full[kb], pol);
+        for (int q = 0; q < PANELS; ++q)
+          tma_load_2d(sB + kb * BS_BYTES + q * B_PANEL, &P.map_b, n0 + 64 * q, kb * BK,
+                      &full[kb], pol);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---- MMA: M = 128 (rows >= L are zero-filled by TMA), N = BNS, K in 16-steps
+    constexpr uint32_t idesc = make_idesc_f16(kBF16, BM, BNS, /*a_mn=*/false, /*b_mn=*/true);
+    for (int kb = 0; kb < P.num_kb; ++kb) {
+      mbar_wait(&full[kb], 0);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t a0 = smem_u32(sA + kb * a_kb);
+        const uint32_t b0 = smem_u32(sB + kb * BS_BYTES);
+#pragma unroll
+        for (int ks = 0; ks < BK / UK; ++ks)
+          tc_mma_f16(tmem_base, make_smem_desc(a0 + ks * (UK * 2), 16, 1024),
+                     make_smem_desc(b0 + ks * (UK * 128), B_PANEL, 1024), idesc,
+                     (kb | ks) != 0 ? 1u : 0u);
+        if (kb + 1 == P.num_kb) tc_commit(done);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) .. (its rows), all BNS columns
+    const uint32_t quad = warp & 3;
+    const int row = static_cast<int>(quad * 32 + lane);
+    uint32_t chk = 0u;
+    griddep_wait();  // the repeated slice is read from x below
+    const bool live = row < P.L;
+    const uint16_t* xrow = static_cast<const uint16_t*>(P.x) +
+                           static_cast<int64_t>(live ? row : 0) * P.ldx + P.rep_base;
+    // every CTA reads the same few rows of x here: issue all of this thread's rep loads
+    // before waiting for the MMAs so their (contended) latency hides behind the loads
+    uint4 xr[BNS / 8];
+#pragma unroll
+    for (int j = 0; j < BNS / 8; ++j) {
+      const int col = n0 + 8 * j;
+      xr[j] = (live && P.has_rep && col < P.N)
+                  ? __ldg(reinterpret_cast<const uint4*>(xrow + (col % P.d_h)))
+                  : make_uint4(0, 0, 0, 0);
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+#pragma unroll
+    for (int c = 0; c < BNS / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem_base + ((quad * 32u) << 16) + c * 32, r);
+      tmem_ld_wait();
+      const int col0 = n0 + c * 32;
+      if (!live || col0 >= P.N) continue;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const int col = col0 + 8 * g;
+        if (col >= P.N) break;
+        const uint4 xv = xr[c * 4 + g];
+        const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 v = add_f32_x16x2<kBF16>(__uint_as_float(r[8 * g + 2 * e]),
+                                               __uint_as_float(r[8 * g + 2 * e + 1]), xw[e]);
+          o[e] = pack2<kBF16>(v.x, v.y);
+          if constexpr (kCheck) chk = max_abs2_nan<kBF16>(chk, o[e]);
+        }
+        uint16_t* dst;
+        if (P.head_major) {
+          const int h = col / P.out_d_h;
+          dst = static_cast<uint16_t*>(P.out) +
+                (static_cast<int64_t>(h) * P.L + row) * P.ldo + (col - h * P.out_d_h);
+        } else {
+          dst = static_cast<uint16_t*>(P.out) + static_cast<int64_t>(row) * P.ldo + col;
+        }
+        *reinterpret_cast<uint4*>(dst) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    if constexpr (kCheck) {
+      if (__any_sync(0xffffffffu, nonfinite2<kBF16>(chk)) && lane == 0) atomicExch(prm.flag, 1);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<1>(tmem_base, BNS);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -773,9 +936,112 @@ int launch_params(const tc::TcParams& prm, int total, bool bf16, bool check,
 
 }  // namespace
 
+// Small-L launch: one CTA per BNS-column block of each problem (no clusters).
+int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStream_t stream) {
+  using namespace tc;
+  int64_t cols = 0, max_l = 1;
+  for (int i = 0; i < count; ++i) {
+    cols += probs[i].N;
+    max_l = probs[i].L > max_l ? probs[i].L : max_l;
+  }
+  const int a_rows = static_cast<int>((max_l + 7) / 8 * 8);
+  const int a_kb_bytes = a_rows * BK * 2;
+  // Column block: 64 when the CTAs that gives fit in one wave at two CTAs per SM, else
+  // 128 (C streams through as many SMs as possible in a single wave)
+  const int per_sm64 = small_smem_bytes(64, a_kb_bytes) * 2 <= 232448 ? 2 : 1;
+  const int bns = (cols + 63) / 64 <= static_cast<int64_t>(per_sm64) * sm_count() ? 64 : 128;
+  TcParams prm{};
+  prm.count = count;
+  prm.flag = flag;
+  prm.a_kb_bytes = a_kb_bytes;
+  int total = 0;
+  for (int i = 0; i < count; ++i) {
+    const Problem& q = probs[i];
+    TcProblem& P = prm.p[i];
+    std::string err;
+    const bool has_rep = q.rep_base >= 0;
+    const auto* xb = static_cast<const uint16_t*>(q.x) + q.mul_base;
+    if (!encode_2d(&P.map_a, xb, bf16, q.K, q.L, q.ldx, BK, a_rows, &err) ||
+        !encode_2d(&P.map_b, q.c, bf16, q.N, q.K, q.ldc, 64, BK, &err)) {
+      set_error(err);
+      return BD_ERR_CUDA;
+    }
+    P.x = q.x;
+    P.ldx = q.ldx;
+    P.L = static_cast<int32_t>(q.L);
+    P.N = static_cast<int32_t>(q.N);
+    P.K = static_cast<int32_t>(q.K);
+    P.d_h = static_cast<int32_t>(has_rep ? q.d_h : 1);
+    P.rep_base = static_cast<int32_t>(has_rep ? q.rep_base : 0);
+    P.has_rep = has_rep ? 1 : 0;
+    P.head_major = q.out_layout == BD_OUT_HEAD_MAJOR ? 1 : 0;
+    P.out_d_h = static_cast<int32_t>(q.d_h);
+    P.out = q.out;
+    P.ldo = q.ldo;
+    P.num_kb = static_cast<int32_t>((q.K + BK - 1) / BK);
+    P.tiles_n = static_cast<int32_t>((q.N + bns - 1) / bns);
+    P.tile_start = total;
+    total += P.tiles_n;
+  }
+  prm.total_tiles = total;
+  if (total == 0) return BD_OK;
+  using KernFn = void (*)(TcParams);
+  static const KernFn kerns[2][2][2] = {
+      {{kv_proj_small_kernel<false, false, 64>, kv_proj_small_kernel<false, false, 128>},
+       {kv_proj_small_kernel<false, true, 64>, kv_proj_small_kernel<false, true, 128>}},
+      {{kv_proj_small_kernel<true, false, 64>, kv_proj_small_kernel<true, false, 128>},
+       {kv_proj_small_kernel<true, true, 64>, kv_proj_small_kernel<true, true, 128>}}};
+  const int vb = bf16 ? 1 : 0, vc = flag != nullptr ? 1 : 0, vn = bns == 128 ? 1 : 0;
+  const KernFn kern = kerns[vb][vc][vn];
+  const size_t smem = small_smem_bytes(bns, a_kb_bytes);
+  static bool attr_done[2][2][2] = {};
+  if (!attr_done[vb][vc][vn]) {  // the largest footprint this variant can ask for
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(small_smem_bytes(bns, A_BYTES)));
+    if (e != cudaSuccess) {
+      set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      return BD_ERR_CUDA;
+    }
+    attr_done[vb][vc][vn] = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(total);
+  cfg.blockDim = dim3(SM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm);
+  note_launch();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("kv_proj_small launch: ") + cudaGetErrorString(e));
+    return BD_ERR_CUDA;
+  }
+  return BD_OK;
+}
+
+// Problems the small-L kernel serves: every problem at most one 128-row tile deep with
+// A resident (K <= 384), and no fused all-gather.
+bool small_eligible(const Problem* probs, int count) {
+  static const bool off = [] {  // BD_SMALL_L=0 routes small L to the persistent kernel
+    const char* e = getenv("BD_SMALL_L");
+    return e != nullptr && atoi(e) == 0;
+  }();
+  if (off) return false;
+  for (int i = 0; i < count; ++i)
+    if (probs[i].L > tc::BM || probs[i].K > tc::SM_MAX_KB * tc::BK || probs[i].world > 0)
+      return false;
+  return true;
+}
+
 int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_t stream) {
   using namespace tc;
   const bool bf16 = dtype == BD_BF16;
+  if (small_eligible(probs, count)) return launch_small(probs, count, bf16, flag, stream);
   TcParams prm;
   {
     const ParamKey key = make_key(probs, count, bf16);

@@ -340,3 +340,25 @@ def test_fused_allgather_single_device_ranks(dtype, world, cuda):
     for p_ in range(2):
         for r in range(world):
             torch.testing.assert_close(gathered[p_][r], full[p_], rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("L", [1, 7, 64, 128])
+def test_small_l_kernel_bit_identical_to_persistent_kernel(dtype, L, cuda):
+    """L <= 128 runs the small-L (decode) kernel; its rows equal, bit for bit, the same
+    rows computed by the persistent kernel inside a longer batch (same FP32 tensor-core
+    accumulation, same FHADD + rounding), for both tags, grouped, and head-major."""
+    d, d_h, n = 512, 128, 16
+    g = torch.Generator().manual_seed(L)
+    x_long = torch.randn(300, d, generator=g).to(dtype).to(cuda)
+    ck = (torch.randn(d - d_h, n * d_h, generator=g) / 8).to(dtype).to(cuda)
+    cv = (torch.randn(d - d_h, n * d_h, generator=g) / 8).to(dtype).to(cuda)
+    specs = [(ck, d_h, n, bd.Tag.FIRST), (cv, d_h, n, bd.Tag.LAST)]
+    k_long, v_long = bd.fused_kv_proj_grouped(x_long, specs)
+    x = x_long[:L].clone()
+    k, v = bd.fused_kv_proj_grouped(x, specs, check_finite=True)
+    torch.testing.assert_close(k, k_long[:L], rtol=0, atol=0)
+    torch.testing.assert_close(v, v_long[:L], rtol=0, atol=0)
+    kh, vh = bd.fused_kv_proj_grouped(x, specs, out_layout="head")
+    torch.testing.assert_close(kh, k.view(L, n, d_h).transpose(0, 1), rtol=0, atol=0)
+    torch.testing.assert_close(vh, v.view(L, n, d_h).transpose(0, 1), rtol=0, atol=0)
