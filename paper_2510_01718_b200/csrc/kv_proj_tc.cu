@@ -111,6 +111,7 @@ struct TcParams {
   int32_t count;
   int32_t total_tiles;  // tiles of (BM * CG) rows x BN columns
   int32_t a_kb_bytes;   // small-L kernel: bytes of one A k-block (rows rounded to 8 x 128 B)
+  int32_t strided;      // tiles dealt round-robin to the pairs (streaming-A problems)
   int* flag;            // non-finite flag (kCheck instantiation only)
 };
 
@@ -132,19 +133,29 @@ struct TileCursor {
   int n_span;    // tiles_n * BN of problem pi
   int pend;      // first tile of problem pi + 1
   int t;
+  int step;      // tile stride between this pair's consecutive tiles (1: contiguous)
 };
 __device__ __forceinline__ void cursor_load(const TcParams& prm, TileCursor& c) {
   c.n_span = prm.p[c.pi].tiles_n * BN;
   c.pend = c.pi + 1 < prm.count ? prm.p[c.pi + 1].tile_start : 0x7fffffff;
 }
-__device__ __forceinline__ TileCursor cursor_at(const TcParams& prm, int t) {
+__device__ __forceinline__ TileCursor cursor_at(const TcParams& prm, int t, int step) {
   TileCursor c;
   c.t = t;
+  c.step = step;
   decode_tile(prm, t, c.pi, c.m0, c.n0);
   cursor_load(prm, c);
   return c;
 }
 __device__ __forceinline__ void cursor_next(const TcParams& prm, TileCursor& c) {
+  if (c.step != 1) {  // round-robin tiles (long K): a full decode is off the critical path
+    c.t += c.step;
+    if (c.t < prm.total_tiles) {
+      decode_tile(prm, c.t, c.pi, c.m0, c.n0);
+      cursor_load(prm, c);
+    }
+    return;
+  }
   ++c.t;
   c.n0 += BN;
   if (c.n0 >= c.n_span) {
@@ -294,8 +305,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int units = static_cast<int>(gridDim.x >> 1);
   // Contiguous tile range per pair: consecutive tiles share the row-block (A resident,
   // rep tile reused); the split is balanced to within one tile.
-  const int t_begin = static_cast<int>(static_cast<int64_t>(unit) * total_tiles / units);
-  const int t_end = static_cast<int>(static_cast<int64_t>(unit + 1) * total_tiles / units);
+  // Tile schedule.  Contiguous ranges per pair (consecutive tiles share the row-block:
+  // A resident, rep tile reused; balanced to within one tile) — or, when A streams
+  // (K > 384, nothing to reuse), round-robin: pair u takes tiles u, u + units, ..., so at
+  // any moment the pairs work on a few adjacent row-blocks and the live set of A and C
+  // stays inside L2 instead of 74 far-apart row-blocks thrashing it.
+  const bool rr = prm.strided != 0;
+  const int t_step = rr ? units : 1;
+  const int t_begin = rr ? unit : static_cast<int>(static_cast<int64_t>(unit) * total_tiles / units);
+  const int t_end = rr ? total_tiles
+                       : static_cast<int>(static_cast<int64_t>(unit + 1) * total_tiles / units);
   // Programmatic dependent launch: everything up to here (barrier init, TMEM allocation,
   // descriptor prefetch) may overlap the tail of the previous kernel in the stream.  Only
   // the threads that read global memory the previous kernel may have written wait for it
@@ -323,7 +342,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         asm volatile("" ::"r"(pi), "r"(m0), "r"(n0), "r"(nkb));
       }
       griddep_wait();
-      for (int t = t_begin; t < t_end; ++t) {
+      for (int t = t_begin; t < t_end; t += t_step) {
         int pi, m0, n0;
         decode_tile(prm, t, pi, m0, n0);
         const TcProblem& P = prm.p[pi];
@@ -374,10 +393,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t a_iter = 0, a_base = 0, b_iter = 0;
       int prev_key = -1;
       int it = 0;
-      TileCursor cur = cursor_at(prm, t_begin);
+      TileCursor cur = cursor_at(prm, t_begin, t_step);
       TileCursor nxt = cur;
       cursor_next(prm, nxt);
-      for (int t = t_begin; t < t_end; ++t, ++it) {
+      for (int t = t_begin; t < t_end; t += t_step, ++it) {
         const int pi = cur.pi;
         const TcProblem& P = prm.p[pi];
         const int num_kb = P.num_kb, num_kbb = P.num_kbb;
@@ -386,7 +405,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool reload_a = stream_a || key != prev_key;
         prev_key = key;
         // Last tile reading this A row-block: release each slot after its k-block's MMAs.
-        const bool last_use = stream_a || t + 1 >= t_end || blk_key(nxt.pi, nxt.m0) != key;
+        const bool last_use =
+            stream_a || t + t_step >= t_end || blk_key(nxt.pi, nxt.m0) != key;
         cur = nxt;
         cursor_next(prm, nxt);
         if (reload_a) {
@@ -477,7 +497,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int cur_key = -1;   // row-block whose rep values are in repv (-1: none)
     uint4 repv[8];      // rep values of this thread's row, columns half*64 + [0, 64) mod d_h
     int it = 0;
-    for (int t = t_begin; t < t_end; ++t, ++it) {
+    for (int t = t_begin; t < t_end; t += t_step, ++it) {
       int pi, m0, n0;
       decode_tile(prm, t, pi, m0, n0);
       const TcProblem& P = prm.p[pi];
@@ -501,7 +521,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         named_bar_sync(2, 32 * EPI_WARPS);  // every epilogue thread holds its rep values
         if (leader) {
-          for (int tn = t + 1; tn < t_end; ++tn) {  // prefetch the next row-block's rep
+          for (int tn = t + t_step; tn < t_end; tn += t_step) {  // next row-block's rep
             int npi, nm0, nn0;
             decode_tile(prm, tn, npi, nm0, nn0);
             if (blk_key(npi, nm0) != key) {
@@ -1134,6 +1154,8 @@ int build_params(const Problem* probs, int count, bool bf16, tc::TcParams& prm,
     total += P.tiles_n * static_cast<int32_t>((q.L + BM * cg - 1) / (BM * cg));
   }
   prm.total_tiles = total;
+  for (int i = 0; i < count; ++i)
+    if (prm.p[i].num_kb > A_SLOTS) prm.strided = 1;
   if (prm.world > 0) {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(stream, &cap);
