@@ -147,8 +147,9 @@ __device__ __forceinline__ TileCursor cursor_at(const TcParams& prm, int t, int 
   cursor_load(prm, c);
   return c;
 }
+template <bool kRR>
 __device__ __forceinline__ void cursor_next(const TcParams& prm, TileCursor& c) {
-  if (c.step != 1) {  // round-robin tiles (long K): a full decode is off the critical path
+  if constexpr (kRR) {  // round-robin tiles (long K): a full decode is off the critical path
     c.t += c.step;
     if (c.t < prm.total_tiles) {
       decode_tile(prm, c.t, c.pi, c.m0, c.n0);
@@ -244,7 +245,8 @@ __device__ __forceinline__ bool nonfinite2(uint32_t w) {
 }
 
 // kCheck: compute the non-finite flag (instantiated only when the caller asked for it).
-template <bool kBF16, bool kCheck>
+// kRR: round-robin tile schedule (streaming-A problems), else contiguous ranges.
+template <bool kBF16, bool kCheck, bool kRR>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     kv_proj_tc_kernel(const __grid_constant__ TcParams prm) {
   extern __shared__ uint8_t smem_raw[];
@@ -310,7 +312,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // (K > 384, nothing to reuse), round-robin: pair u takes tiles u, u + units, ..., so at
   // any moment the pairs work on a few adjacent row-blocks and the live set of A and C
   // stays inside L2 instead of 74 far-apart row-blocks thrashing it.
-  const bool rr = prm.strided != 0;
+  constexpr bool rr = kRR;
   const int t_step = rr ? units : 1;
   const int t_begin = rr ? unit : static_cast<int>(static_cast<int64_t>(unit) * total_tiles / units);
   const int t_end = rr ? total_tiles
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int it = 0;
       TileCursor cur = cursor_at(prm, t_begin, t_step);
       TileCursor nxt = cur;
-      cursor_next(prm, nxt);
+      cursor_next<kRR>(prm, nxt);
       for (int t = t_begin; t < t_end; t += t_step, ++it) {
         const int pi = cur.pi;
         const TcProblem& P = prm.p[pi];
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool last_use =
             stream_a || t + t_step >= t_end || blk_key(nxt.pi, nxt.m0) != key;
         cur = nxt;
-        cursor_next(prm, nxt);
+        cursor_next<kRR>(prm, nxt);
         if (reload_a) {
           a_base = a_iter;
           a_iter += num_kb;
@@ -1183,18 +1185,23 @@ int launch_params(const tc::TcParams& prm, int total, bool bf16, bool check,
   using namespace tc;
   constexpr int cg = CG;
   using KernFn = void (*)(TcParams);
-  KernFn kern = bf16 ? (check ? kv_proj_tc_kernel<true, true> : kv_proj_tc_kernel<true, false>)
-                     : (check ? kv_proj_tc_kernel<false, true> : kv_proj_tc_kernel<false, false>);
+  static const KernFn kerns[2][2][2] = {
+      {{kv_proj_tc_kernel<false, false, false>, kv_proj_tc_kernel<false, false, true>},
+       {kv_proj_tc_kernel<false, true, false>, kv_proj_tc_kernel<false, true, true>}},
+      {{kv_proj_tc_kernel<true, false, false>, kv_proj_tc_kernel<true, false, true>},
+       {kv_proj_tc_kernel<true, true, false>, kv_proj_tc_kernel<true, true, true>}}};
+  const int vb = bf16 ? 1 : 0, vc = check ? 1 : 0, vr = prm.strided ? 1 : 0;
+  KernFn kern = kerns[vb][vc][vr];
   const size_t smem = SMEM_BYTES;
-  static bool attr_set[2][2] = {{false, false}, {false, false}};
-  if (!attr_set[bf16 ? 1 : 0][check ? 1 : 0]) {
+  static bool attr_set[2][2][2] = {};
+  if (!attr_set[vb][vc][vr]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) {
       set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
       return BD_ERR_CUDA;
     }
-    attr_set[bf16 ? 1 : 0][check ? 1 : 0] = true;
+    attr_set[vb][vc][vr] = true;
   }
   const int units = sm_count() / cg;
   const int grid_units = total < units ? total : units;
