@@ -256,13 +256,25 @@ def bd_mla_forward(hidden: torch.Tensor, w: BDMLAWeights, *, causal: bool = True
     With head-sharded weights (``shard_bd_mla``) the partial outputs are summed with one
     all_reduce over ``group``."""
     cfg, H = w.cfg, w.n_heads
+    L = hidden.shape[0]
     q_nope, q_pe = _split_q(hidden @ w.w_q, H, cfg)
     c_kv, k_pe = _latent(hidden, w.w_kva, w.kva_norm, cfg)
-    k_nope, v = fused_kv_proj_grouped(c_kv, [(w.c_qk, cfg.qk_nope, H, w.qk_tag),
-                                             (w.c_vo, cfg.v_head, H, w.vo_tag)])
     rope = lambda t: _rope(t, cfg.rope_theta, cfg.rope_interleaved)  # noqa: E731
-    o = _mla_attend(q_nope, rope(q_pe), k_nope, rope(k_pe), v,
-                    H, cfg, causal)
+    # The BD kernel writes K'_nope head-major straight into the first qk_nope columns of
+    # the attention key buffer [H, L, nope + rope] (row stride nope + rope) and V'
+    # head-major into [H, L, v]: the SDPA operands need no transpose or concatenation
+    # copy of K'/V'; only the shared RoPE key part is broadcast into each head's tail.
+    k_buf = torch.empty((H, L, cfg.qk_head), dtype=c_kv.dtype, device=c_kv.device)
+    v_buf = torch.empty((H, L, cfg.v_head), dtype=c_kv.dtype, device=c_kv.device)
+    fused_kv_proj_grouped(c_kv, [(w.c_qk, cfg.qk_nope, H, w.qk_tag),
+                                 (w.c_vo, cfg.v_head, H, w.vo_tag)],
+                          outs=[k_buf[..., :cfg.qk_nope], v_buf], out_layout="head")
+    k_buf[..., cfg.qk_nope:] = rope(k_pe)[None]
+    q = torch.cat([q_nope.view(L, H, cfg.qk_nope), rope(q_pe).view(L, H, cfg.qk_rope)], -1)
+    with sdpa_kernel(_BACKENDS):
+        o = F.scaled_dot_product_attention(q.transpose(0, 1)[None], k_buf[None], v_buf[None],
+                                           is_causal=causal, scale=1.0 / math.sqrt(cfg.qk_head))
+    o = o[0].transpose(0, 1).reshape(L, H * cfg.v_head)
     out = o @ w.b_vo
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(out, group=group)
