@@ -205,9 +205,16 @@ def bda_forward(x: torch.Tensor, w: BDAWeights, *, causal: bool = False,
     """
     _check_input(x, w.d, w.precision)
     q = _proj(x, w.b_qk)
-    k, v = fused_kv_proj_grouped(x, [(w.c_qk, w.d_h, w.n_heads, w.qk_tag),
-                                     (w.c_vo, w.d_h, w.n_heads, w.vo_tag)],
-                                 check_finite=check_finite)
+    specs = [(w.c_qk, w.d_h, w.n_heads, w.qk_tag), (w.c_vo, w.d_h, w.n_heads, w.vo_tag)]
+    if x.dtype in (torch.float16, torch.bfloat16) and w.d_h % 64 == 0:
+        # K', V' head-major [H, L, d_h]: SDPA's [1, H, L, d_h] operands, no transpose copy
+        kh, vh = fused_kv_proj_grouped(x, specs, check_finite=check_finite, out_layout="head")
+        L, H = x.shape[0], w.n_heads
+        qh = q.view(L, H, w.d_h).transpose(0, 1)[None]
+        o = F.scaled_dot_product_attention(qh, kh[None], vh[None], is_causal=causal,
+                                           scale=1.0 / math.sqrt(w.d_h))
+        return _proj(o[0].transpose(0, 1).reshape(L, H * w.d_h), w.b_vo)
+    k, v = fused_kv_proj_grouped(x, specs, check_finite=check_finite)
     return _proj(_attend(q, k, v, w.n_heads, w.d_h, causal), w.b_vo)
 
 
