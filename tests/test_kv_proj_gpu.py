@@ -362,3 +362,28 @@ def test_small_l_kernel_bit_identical_to_persistent_kernel(dtype, L, cuda):
     kh, vh = bd.fused_kv_proj_grouped(x, specs, out_layout="head")
     torch.testing.assert_close(kh, k.view(L, n, d_h).transpose(0, 1), rtol=0, atol=0)
     torch.testing.assert_close(vh, v.view(L, n, d_h).transpose(0, 1), rtol=0, atol=0)
+
+
+def test_launch_parameter_cache_follows_buffers(cuda):
+    """The C library caches encoded launch parameters per buffer signature: alternating
+    calls over different buffers (same shapes), strides, layouts, tags and flag pointers
+    must each compute their own result (no stale tensor maps or flag pointers)."""
+    L, d, d_h, n = 700, 512, 128, 16
+    g = torch.Generator().manual_seed(21)
+    xs = [torch.randn(L, d, generator=g).half().to(cuda) for _ in range(3)]
+    cs = [(torch.randn(d - d_h, n * d_h, generator=g) / 8).half().to(cuda) for _ in range(2)]
+    ref = {(i, j, t): bd.fused_kv_proj(xs[i], cs[j], d_h, n, t, check_finite=False)
+           for i in range(3) for j in range(2) for t in bd.Tag}
+    for rnd in range(3):  # > cache size distinct signatures, revisited
+        for (i, j, t), want in ref.items():
+            out = torch.empty(L, n * d_h + 64, dtype=torch.half, device=cuda)[:, :n * d_h] \
+                if (i + j + rnd) % 2 else None
+            got = bd.fused_kv_proj(xs[i], cs[j], d_h, n, t, out=out, check_finite=(rnd == 1))
+            torch.testing.assert_close(got, want, rtol=0, atol=0)
+    # the non-finite flag of a cached signature still reaches the kernel
+    bad = xs[0].clone()
+    bad[5, 300] = float("inf")
+    with pytest.raises(ValueError):
+        bd.fused_kv_proj(bad, cs[0], d_h, n, bd.Tag.FIRST, check_finite=True)
+    with pytest.raises(ValueError):
+        bd.fused_kv_proj(bad, cs[0], d_h, n, bd.Tag.FIRST, check_finite=True)
