@@ -17,3 +17,11 @@ for chunks in (1, 2, 4, 8):
 ref = bd.fused_kv_proj_grouped(xh[0].to(dev), specs)
 out = bd.fused_kv_proj_grouped_host(xh[0], specs, chunks=4)
 print("equal:", torch.equal(out[0].to(dev), ref[0]), torch.equal(out[1].to(dev), ref[1]))
+# raw copy-engine ceiling on this box: one 67 MB D2H and one 8 MB H2D, pinned
+src = torch.empty(L, 4096, dtype=torch.half, device=dev)
+dst = torch.empty(L, 4096, dtype=torch.half).pin_memory()
+for _ in range(3): dst.copy_(src, non_blocking=True)
+torch.cuda.synchronize(); t = time.perf_counter()
+for _ in range(20): dst.copy_(src, non_blocking=True)
+torch.cuda.synchronize(); dt = (time.perf_counter() - t) / 20
+print(f"D2H {src.numel()*2/1e6:.0f} MB: {dt*1e3:.3f} ms  {src.numel()*2/dt/1e9:.1f} GB/s")
