@@ -209,17 +209,17 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int sm_count() {
-  static int cached_dev = -1;
-  static int cached = 0;
+  static std::atomic<int> cached[64] = {};  // per device ordinal, 0 = not queried yet
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev != cached_dev) {
-    int n = 0;
+  if (dev < 0 || dev >= 64) dev = 0;
+  int n = cached[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    cached = n > 0 ? n : 148;
-    cached_dev = dev;
+    n = n > 0 ? n : 148;
+    cached[dev].store(n, std::memory_order_relaxed);
   }
-  return cached;
+  return n;
 }
 
 }  // namespace bdk

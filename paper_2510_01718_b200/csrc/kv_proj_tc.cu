@@ -44,6 +44,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -1016,15 +1017,18 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
   const int vb = bf16 ? 1 : 0, vc = flag != nullptr ? 1 : 0, vn = bns == 128 ? 1 : 0;
   const KernFn kern = kerns[vb][vc][vn];
   const size_t smem = small_smem_bytes(bns, a_kb_bytes);
-  static bool attr_done[2][2][2] = {};
-  if (!attr_done[vb][vc][vn]) {  // the largest footprint this variant can ask for
+  static std::atomic<bool> attr_done[2][2][2] = {};
+  static std::mutex attr_mu;
+  if (!attr_done[vb][vc][vn].load(std::memory_order_acquire)) {
+    std::lock_guard<std::mutex> lock(attr_mu);
+    // the largest footprint this variant can ask for
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(small_smem_bytes(bns, A_BYTES)));
     if (e != cudaSuccess) {
       set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
       return BD_ERR_CUDA;
     }
-    attr_done[vb][vc][vn] = true;
+    attr_done[vb][vc][vn].store(true, std::memory_order_release);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(total);
@@ -1193,15 +1197,17 @@ int launch_params(const tc::TcParams& prm, int total, bool bf16, bool check,
   const int vb = bf16 ? 1 : 0, vc = check ? 1 : 0, vr = prm.strided ? 1 : 0;
   KernFn kern = kerns[vb][vc][vr];
   const size_t smem = SMEM_BYTES;
-  static bool attr_set[2][2][2] = {};
-  if (!attr_set[vb][vc][vr]) {
+  static std::atomic<bool> attr_set[2][2][2] = {};
+  static std::mutex attr_mu;
+  if (!attr_set[vb][vc][vr].load(std::memory_order_acquire)) {
+    std::lock_guard<std::mutex> lock(attr_mu);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) {
       set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
       return BD_ERR_CUDA;
     }
-    attr_set[vb][vc][vr] = true;
+    attr_set[vb][vc][vr].store(true, std::memory_order_release);
   }
   const int units = sm_count() / cg;
   const int grid_units = total < units ? total : units;
