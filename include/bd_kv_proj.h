@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define BD_KV_PROJ_ABI_VERSION 4
+#define BD_KV_PROJ_ABI_VERSION 5
 
 /* element types */
 enum bd_dtype { BD_F32 = 0, BD_F64 = 1, BD_F16 = 2, BD_BF16 = 3 };
@@ -163,6 +163,21 @@ int bd_kv_proj_grouped_ex(const bd_kv_problem* problems, int count, int dtype, i
 int bd_kv_proj_grouped_allgather(const bd_kv_problem* problems, int count, int dtype, int mode,
                                  int world, int rank, void* const* gathered,
                                  int* nonfinite_flag, void* stream);
+
+/*
+ * Projections of the RMS-normalised latent with the norm FUSED (DeepSeek-V2's
+ * kv_a_layernorm in front of kv_b_proj).  x is the RAW latent (L x d); each problem
+ * computes the BD projection of  x_n = x * rsqrt(mean(x[i, :]^2) + eps) * gamma  as
+ *   out[i, j] = r_i * (sum_k x[i, mul_base + k] c_g[k, j] + rep_gamma[j % d_h] x[i, rep_base + j % d_h])
+ * where c_g = diag(gamma[mul_base : mul_base + d - d_h]) c is folded by the caller once per
+ * weight and rep_gamma[p] = gamma[rep_base : rep_base + d_h] (d_h floats, device memory).
+ * The mean runs over the row's d columns.  No separate normalisation pass: one read of x.
+ * Tensor-core path: d_h in {64, 128} and d - d_h <= 384 (the row is resident in smem).
+ * Extends (ref: pkg/src/bdattn/attention.py:249-270) to the MLA latent of SURVEY §8(f) #3.
+ */
+int bd_kv_proj_grouped_rmsnorm(const bd_kv_problem* problems, int count, int dtype, int mode,
+                               int out_layout, const float* const* rep_gamma, float eps,
+                               int* nonfinite_flag, void* stream);
 
 /* Human-readable description of the last error on this thread ("" if none). */
 const char* bd_last_error(void);

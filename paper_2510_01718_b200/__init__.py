@@ -39,8 +39,10 @@ from .decompose import (
 from .errors import NativeLibraryError, PrecisionError, ShapeError
 from .kv_proj import (
     flop_ratio,
+    fold_rmsnorm,
     fused_kv_proj,
     fused_kv_proj_grouped,
+    fused_rmsnorm_kv_proj_grouped,
     fused_kv_proj_grouped_host,
     fused_kv_proj_host,
     kv_flops,

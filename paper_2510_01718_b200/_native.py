@@ -22,7 +22,7 @@ BD_F32, BD_F64, BD_F16, BD_BF16 = 0, 1, 2, 3
 BD_OK, BD_ERR_SHAPE, BD_ERR_DTYPE, BD_ERR_ALIGN, BD_ERR_CUDA, BD_ERR_ARG = 0, 1, 2, 3, 4, 5
 BD_MODE_AUTO, BD_MODE_EXACT, BD_MODE_TC = 0, 1, 2
 BD_MAX_GROUP = 4
-ABI_VERSION = 4
+ABI_VERSION = 5
 BD_MAX_PEERS = 8
 BD_OUT_TOKEN_MAJOR, BD_OUT_HEAD_MAJOR = 0, 1
 BD_TAG_FIRST, BD_TAG_LAST = 0, 1
@@ -32,6 +32,7 @@ EXPORTED_SYMBOLS = (
     "bd_kv_proj_grouped",
     "bd_kv_proj_grouped_ex",
     "bd_kv_proj_grouped_allgather",
+    "bd_kv_proj_grouped_rmsnorm",
     "bd_kv_proj_host",
     "bd_matmul",
     "bd_linear_forward",
@@ -87,6 +88,9 @@ def load() -> ctypes.CDLL:
     lib.bd_kv_proj_grouped_allgather.argtypes = [ctypes.POINTER(KvProblem), ci, ci, ci, ci, ci,
                                                  ctypes.POINTER(vp), vp, vp]
     lib.bd_kv_proj_grouped_allgather.restype = ci
+    lib.bd_kv_proj_grouped_rmsnorm.argtypes = [ctypes.POINTER(KvProblem), ci, ci, ci, ci,
+                                               ctypes.POINTER(vp), ctypes.c_float, vp, vp]
+    lib.bd_kv_proj_grouped_rmsnorm.restype = ci
     lib.bd_kv_proj_host.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, ci, ci,
                                     ctypes.POINTER(ctypes.c_int)]
     lib.bd_kv_proj_host.restype = ci

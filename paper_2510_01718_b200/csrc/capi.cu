@@ -129,7 +129,8 @@ int dispatch(const Problem* probs, int count, int dtype, int m, int* flag, cudaS
 
 int run_group(const bd_kv_problem* probs, int count, int dtype, int mode, int* flag,
               cudaStream_t stream, int out_layout = BD_OUT_TOKEN_MAJOR, int world = 0,
-              int rank = 0, void* const* gathered = nullptr) {
+              int rank = 0, void* const* gathered = nullptr,
+              const float* const* rep_gamma = nullptr, float eps = 0.f) {
   if (out_layout != BD_OUT_TOKEN_MAJOR && out_layout != BD_OUT_HEAD_MAJOR)
     return fail(BD_ERR_ARG, "unknown out_layout " + std::to_string(out_layout));
   if (probs == nullptr || count < 1 || count > BD_MAX_GROUP)
@@ -143,6 +144,16 @@ int run_group(const bd_kv_problem* probs, int count, int dtype, int mode, int* f
     rc = validate(probs[i], dtype, m, i, out_layout);
     if (rc != BD_OK) return rc;
     ps[i] = to_problem(probs[i], out_layout);
+    if (rep_gamma != nullptr) {
+      if (rep_gamma[i] == nullptr) return fail(BD_ERR_ARG, "null rep_gamma");
+      const bool first = probs[i].mul_base == probs[i].d_h && probs[i].rep_base == 0;
+      const bool last = probs[i].mul_base == 0 && probs[i].rep_base == probs[i].d - probs[i].d_h;
+      if (!first && !last)
+        return fail(BD_ERR_SHAPE, "fused RMSNorm: the multiplied and repeated slices must "
+                                  "partition the row (tags FIRST / LAST)");
+      ps[i].rep_gamma = rep_gamma[i];
+      ps[i].norm_eps = eps;
+    }
     if (world > 0) {
       ps[i].world = world;
       ps[i].head0 = static_cast<int32_t>(rank * probs[i].n_heads);
@@ -262,6 +273,16 @@ int bd_kv_proj_grouped_allgather(const bd_kv_problem* problems, int count, int d
   }
   return run_group(local, count, dtype, mode, nonfinite_flag, static_cast<cudaStream_t>(stream),
                    BD_OUT_HEAD_MAJOR, world, rank, gathered);
+}
+
+int bd_kv_proj_grouped_rmsnorm(const bd_kv_problem* problems, int count, int dtype, int mode,
+                               int out_layout, const float* const* rep_gamma, float eps,
+                               int* nonfinite_flag, void* stream) {
+  using namespace bdk;
+  if (rep_gamma == nullptr) return fail(BD_ERR_ARG, "null rep_gamma array");
+  if (!(eps >= 0.f)) return fail(BD_ERR_ARG, "eps must be >= 0");
+  return run_group(problems, count, dtype, mode, nonfinite_flag,
+                   static_cast<cudaStream_t>(stream), out_layout, 0, 0, nullptr, rep_gamma, eps);
 }
 
 int bd_kv_proj_host(const void* x, const void* c, void* out, int64_t L, int64_t d, int64_t d_h,

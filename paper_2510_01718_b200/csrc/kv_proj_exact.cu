@@ -116,12 +116,32 @@ __global__ void __launch_bounds__(EX_THREADS)
   for (int i = 0; i < 4; ++i) {
     const int64_t row = m0 + ty * 4 + i;
     if (row >= P.L) continue;
+    // fused RMSNorm: r = 1 / sqrt(mean(x[row, 0:d]^2) + eps), d = K + d_h (the multiplied
+    // and repeated slices partition the row); out = r * (acc + gamma_rep * x_rep)
+    T rn = T(1);
+    if (P.rep_gamma != nullptr) {
+      T ss = T(0);
+      const int64_t dfull = K + P.d_h;
+      for (int64_t k = 0; k < dfull; ++k) {
+        const T xv = x[row * P.ldx + k];
+        ss = ExactOps<T>::add(ss, ExactOps<T>::mul(xv, xv));
+      }
+      rn = T(1) / sqrt(ss / static_cast<T>(dfull) + static_cast<T>(P.norm_eps));
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t col = n0 + tx * 4 + j;
       if (col >= N) continue;
-      const T v = has_rep ? ExactOps<T>::add(acc[i][j], x[row * P.ldx + P.rep_base + (col % P.d_h)])
-                          : acc[i][j];
+      T v;
+      if (P.rep_gamma != nullptr) {
+        const T xr = x[row * P.ldx + P.rep_base + (col % P.d_h)];
+        v = ExactOps<T>::mul(
+            rn, ExactOps<T>::add(acc[i][j],
+                                 ExactOps<T>::mul(static_cast<T>(P.rep_gamma[col % P.d_h]), xr)));
+      } else {
+        v = has_rep ? ExactOps<T>::add(acc[i][j], x[row * P.ldx + P.rep_base + (col % P.d_h)])
+                    : acc[i][j];
+      }
       if (P.world > 0) {  // fused all-gather: every rank's full-width head-major buffer
         const int64_t off = ((P.head0 + col / P.d_h) * P.L + row) * P.ldo + col % P.d_h;
         for (int r = 0; r < P.world; ++r) static_cast<T*>(P.peers[r])[off] = v;

@@ -29,6 +29,11 @@ struct Problem {
   int32_t world;
   int32_t head0;
   void* peers[BD_MAX_PEERS];
+  // Fused RMSNorm (rep_gamma != null): x is the raw latent; out = r_i * (x[:, mul] c +
+  // rep_gamma * x[:, rep]) with r_i = rsqrt(mean(x[i, :d]^2) + norm_eps), d = K + d_h
+  // (c must carry the multiplied columns' norm weight, folded by the caller).
+  const float* rep_gamma;
+  float norm_eps;
 };
 
 // Thread-local error text set by the launchers; returned by bd_last_error().

@@ -77,8 +77,9 @@ constexpr uint32_t REP_BYTES = 2 * REP_BOX;   // d_h <= 128 -> at most two boxes
 constexpr uint32_t STG_BYTES = 32 * 64 * 2;   // output staging box: 32 rows x 64 cols (SW128)
 constexpr int STG_BUFS = 1;                   // per-warp staging buffers
 constexpr uint32_t TMEM_COLS = 512;          // NUM_ACC accumulator buffers
+constexpr uint32_t NORM_SCRATCH = 2 * BM * 4;  // kNorm: per-row partial sums of squares
 constexpr size_t SMEM_BYTES = 1024 + A_SLOTS * A_BYTES + B_STAGES * B_BYTES + REP_BYTES +
-                              EPI_WARPS * STG_BUFS * STG_BYTES + 512;
+                              EPI_WARPS * STG_BUFS * STG_BYTES + 512 + NORM_SCRATCH;
 static_assert((2 * A_SLOTS + 2 * B_STAGES + 2 * NUM_ACC + 1) * 8 + 4 <= 512, "barrier area");
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
@@ -98,6 +99,9 @@ struct TcProblem {
   int32_t out_d_h;      // head width of the head-major output
   void* out;            // output base and row stride (the small-L kernel stores directly)
   int64_t ldo;
+  const float* rep_gamma;  // kNorm: RMSNorm weight of the repeated slice (d_h floats)
+  float norm_eps;          // kNorm: RMSNorm epsilon
+  int32_t norm_d;          // kNorm: columns of x's row (K + d_h) the norm averages over
 };
 
 struct TcParams {
@@ -113,6 +117,7 @@ struct TcParams {
   int32_t total_tiles;  // tiles of (BM * CG) rows x BN columns
   int32_t a_kb_bytes;   // small-L kernel: bytes of one A k-block (rows rounded to 8 x 128 B)
   int32_t strided;      // tiles dealt round-robin to the pairs (streaming-A problems)
+  int32_t norm;         // fused RMSNorm (kNorm variant)
   int* flag;            // non-finite flag (kCheck instantiation only)
 };
 
@@ -247,7 +252,8 @@ __device__ __forceinline__ bool nonfinite2(uint32_t w) {
 
 // kCheck: compute the non-finite flag (instantiated only when the caller asked for it).
 // kRR: round-robin tile schedule (streaming-A problems), else contiguous ranges.
-template <bool kBF16, bool kCheck, bool kRR>
+// kNorm: x is the raw latent and its RMSNorm is fused (see the epilogue).
+template <bool kBF16, bool kCheck, bool kRR, bool kNorm = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     kv_proj_tc_kernel(const __grid_constant__ TcParams prm) {
   extern __shared__ uint8_t smem_raw[];
@@ -265,6 +271,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tempty = tfull + NUM_ACC;
   uint64_t* rfull = tempty + NUM_ACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 1);
+  float* norm_part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(a_full) + 512);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -277,7 +284,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < A_SLOTS; ++s) {
       mbar_init(&a_full[s], 1);   // armed by the leader's producer with the pair's bytes
-      mbar_init(&a_empty[s], 1);  // one multicast tcgen05.commit
+      // one multicast tcgen05.commit (+ kNorm: this CTA's epilogue, done reading the slot)
+      mbar_init(&a_empty[s], kNorm ? 2 : 1);
     }
     for (int s = 0; s < B_STAGES; ++s) {
       mbar_init(&b_full[s], 1);
@@ -499,6 +507,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t rep_loads = 0;
     int cur_key = -1;   // row-block whose rep values are in repv (-1: none)
     uint4 repv[8];      // rep values of this thread's row, columns half*64 + [0, 64) mod d_h
+    float rnorm = 1.0f;         // kNorm: 1 / RMS of this thread's row
+    bool norm_pending = false;  // kNorm: a new row-block's norm is still to be computed
+    uint32_t ep_a_iter = 0, ep_a_base = 0;  // kNorm: mirror of the MMA's A-slot sequence
     int it = 0;
     for (int t = t_begin; t < t_end; t += t_step, ++it) {
       int pi, m0, n0;
@@ -514,6 +525,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(rfull, rep_loads & 1u);
         ++rep_loads;
         cur_key = key;
+        if constexpr (kNorm) {
+          norm_pending = true;
+          ep_a_base = ep_a_iter;
+          ep_a_iter += static_cast<uint32_t>(P.num_kb);
+        }
         const int dm = P.d_h - 1;
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
@@ -538,6 +554,65 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t acc_phase = (it / NUM_ACC) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if constexpr (kNorm) {
+        if (norm_pending) {
+          // Fused RMSNorm of x (DeepSeek kv_a_layernorm): the row's sum of squares from
+          // the resident A k-blocks (all landed: this tile's MMAs read them) and the rep
+          // values in registers; the two warps of a quadrant split the row and meet in
+          // shared memory.  Then out = r * (sum_k x c_g + gamma_rep x_rep) is evaluated as
+          // (r * acc) + fp16(r * gamma_rep * x_rep): the rep registers are rescaled here.
+          norm_pending = false;
+          float ss = 0.f;
+          const int nkb = P.num_kb;
+          for (int kb = static_cast<int>(half) * 3; kb < nkb && kb < static_cast<int>(half) * 3 + 3;
+               ++kb) {
+            const uint8_t* arow =
+                sA + ((ep_a_base + static_cast<uint32_t>(kb)) % A_SLOTS) * A_BYTES + row_t * 128;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+              const uint4 q = *reinterpret_cast<const uint4*>(arow + ((ch ^ (row_t & 7)) << 4));
+              const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = unpack2<kBF16>(w[e]);
+                ss = fmaf(f.x, f.x, fmaf(f.y, f.y, ss));
+              }
+            }
+          }
+          if (half == 0 || P.d_h > 64) {  // the rep columns, each counted once
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              const uint32_t w[4] = {repv[g].x, repv[g].y, repv[g].z, repv[g].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = unpack2<kBF16>(w[e]);
+                ss = fmaf(f.x, f.x, fmaf(f.y, f.y, ss));
+              }
+            }
+          }
+          norm_part[half * BM + row_t] = ss;
+          named_bar_sync(3, 32 * EPI_WARPS);
+          const float tot = norm_part[row_t] + norm_part[BM + row_t];
+          rnorm = rsqrtf(tot / static_cast<float>(P.norm_d) + P.norm_eps);
+          named_bar_sync(3, 32 * EPI_WARPS);  // everyone read the A slots and the partials
+          if (leader)
+            for (int kb = 0; kb < nkb; ++kb)
+              mbar_arrive(&a_empty[(ep_a_base + static_cast<uint32_t>(kb)) % A_SLOTS]);
+          const int dm = P.d_h - 1;
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            const int jj = (static_cast<int>(half) * 64 + 8 * g) & dm;
+            uint32_t w[4] = {repv[g].x, repv[g].y, repv[g].z, repv[g].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = unpack2<kBF16>(w[e]);
+              w[e] = pack2<kBF16>(rnorm * __ldg(P.rep_gamma + jj + 2 * e) * f.x,
+                                  rnorm * __ldg(P.rep_gamma + jj + 2 * e + 1) * f.y);
+            }
+            repv[g] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
       const int64_t grow = static_cast<int64_t>(my_m0) + row_t;
       const bool has_rep = P.has_rep != 0;
       const uint16_t* xrow = static_cast<const uint16_t*>(P.x) +
@@ -587,8 +662,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int e = 0; e < 4; ++e) {
             // + rep in FP32 with one mixed-precision FHADD per element (exact widening of
             // the 16-bit rep, one FP32 rounding), then one rounding to 16 bit
-            const float2 v = add_f32_x16x2<kBF16>(__uint_as_float(r[8 * g + 2 * e]),
-                                                 __uint_as_float(r[8 * g + 2 * e + 1]), xw[e]);
+            float a0 = __uint_as_float(r[8 * g + 2 * e]);
+            float a1 = __uint_as_float(r[8 * g + 2 * e + 1]);
+            if constexpr (kNorm) {
+              a0 *= rnorm;
+              a1 *= rnorm;
+            }
+            const float2 v = add_f32_x16x2<kBF16>(a0, a1, xw[e]);
             o[e] = pack2<kBF16>(v.x, v.y);
             if constexpr (kCheck) chk = max_abs2_nan<kBF16>(chk, o[e]);
           }
@@ -948,6 +1028,8 @@ ParamKey make_key(const Problem* probs, int count, bool bf16) {
     d.world = q.world;
     d.head0 = q.head0;
     for (int r = 0; r < q.world && r < BD_MAX_PEERS; ++r) d.peers[r] = q.peers[r];
+    d.rep_gamma = q.rep_gamma;
+    d.norm_eps = q.norm_eps;
   }
   return k;
 }
@@ -1059,7 +1141,8 @@ bool small_eligible(const Problem* probs, int count) {
   }();
   if (off) return false;
   for (int i = 0; i < count; ++i)
-    if (probs[i].L > tc::BM || probs[i].K > tc::SM_MAX_KB * tc::BK || probs[i].world > 0)
+    if (probs[i].L > tc::BM || probs[i].K > tc::SM_MAX_KB * tc::BK || probs[i].world > 0 ||
+        probs[i].rep_gamma != nullptr)
       return false;
   return true;
 }
@@ -1134,6 +1217,17 @@ int build_params(const Problem* probs, int count, bool bf16, tc::TcParams& prm,
     P.rep_fast = rep_fast ? 1 : 0;
     P.has_rep = has_rep ? 1 : 0;
     P.head_major = q.out_layout == BD_OUT_HEAD_MAJOR ? 1 : 0;
+    if (q.rep_gamma != nullptr) {
+      // fused RMSNorm: the row must be resident (A k-blocks + staged rep = all d columns)
+      if (!rep_fast || K > A_SLOTS * BK) {
+        set_error("fused RMSNorm needs d_h in {64, 128} and d - d_h <= 384 on the tensor-core path");
+        return BD_ERR_SHAPE;
+      }
+      prm.norm = 1;
+      P.rep_gamma = q.rep_gamma;
+      P.norm_eps = q.norm_eps;
+      P.norm_d = static_cast<int32_t>(K + d_h);
+    }
     if (q.world > 0) {
       prm.world = q.world;
       prm.head0[i] = q.head0;
@@ -1194,10 +1288,13 @@ int launch_params(const tc::TcParams& prm, int total, bool bf16, bool check,
        {kv_proj_tc_kernel<false, true, false>, kv_proj_tc_kernel<false, true, true>}},
       {{kv_proj_tc_kernel<true, false, false>, kv_proj_tc_kernel<true, false, true>},
        {kv_proj_tc_kernel<true, true, false>, kv_proj_tc_kernel<true, true, true>}}};
-  const int vb = bf16 ? 1 : 0, vc = check ? 1 : 0, vr = prm.strided ? 1 : 0;
-  KernFn kern = kerns[vb][vc][vr];
+  static const KernFn kerns_norm[2][2] = {
+      {kv_proj_tc_kernel<false, false, false, true>, kv_proj_tc_kernel<false, true, false, true>},
+      {kv_proj_tc_kernel<true, false, false, true>, kv_proj_tc_kernel<true, true, false, true>}};
+  const int vb = bf16 ? 1 : 0, vc = check ? 1 : 0, vr = prm.norm ? 2 : (prm.strided ? 1 : 0);
+  KernFn kern = vr == 2 ? kerns_norm[vb][vc] : kerns[vb][vc][vr];
   const size_t smem = SMEM_BYTES;
-  static std::atomic<bool> attr_set[2][2][2] = {};
+  static std::atomic<bool> attr_set[2][2][3] = {};
   static std::mutex attr_mu;
   if (!attr_set[vb][vc][vr].load(std::memory_order_acquire)) {
     std::lock_guard<std::mutex> lock(attr_mu);

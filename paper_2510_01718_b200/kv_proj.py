@@ -191,6 +191,63 @@ def fused_kv_proj_grouped(x: torch.Tensor,
     return results
 
 
+def fold_rmsnorm(c: torch.Tensor, gamma: torch.Tensor, d_h: int,
+                 tag: Tag) -> tuple[torch.Tensor, torch.Tensor]:
+    """Offline fold of an RMSNorm weight into a BD coefficient matrix.
+
+    For x_n = RMSNorm(x) * gamma the projection's multiplied term is
+    x_n[:, mul] @ c = r * x[:, mul] @ (diag(gamma[mul]) c): returns (c_g, rep_gamma) with
+    c_g = diag(gamma[mul_base : mul_base + K]) c (rounded once to c's dtype) and
+    rep_gamma = gamma[rep_base : rep_base + d_h] in float32, the arguments of
+    ``fused_rmsnorm_kv_proj_grouped``.
+    """
+    K = int(c.shape[0])
+    d = K + d_h
+    if gamma.dim() != 1 or int(gamma.shape[0]) != d:
+        raise ShapeError(f"gamma must have d = {d} entries")
+    mul_base, rep_base = tag_offsets(d, d_h, tag)
+    g = gamma.to(device=c.device, dtype=torch.float64)
+    c_g = (g[mul_base:mul_base + K, None] * c.to(torch.float64)).to(c.dtype).contiguous()
+    return c_g, g[rep_base:rep_base + d_h].to(torch.float32).contiguous()
+
+
+def fused_rmsnorm_kv_proj_grouped(x: torch.Tensor,
+                                  specs: Sequence[tuple[torch.Tensor, torch.Tensor, int, int, Tag]],
+                                  eps: float, *, outs: Sequence[torch.Tensor] | None = None,
+                                  check_finite: bool = False, mode: str = "auto",
+                                  out_layout: str = "token") -> list[torch.Tensor]:
+    """K'/V' of the RMS-normalised latent in ONE launch, the norm fused (one read of x).
+
+    ``x`` is the raw latent (e.g. DeepSeek-V2's compressed kv before kv_a_layernorm);
+    ``specs`` are (c_g, rep_gamma, d_h, n_heads, tag) with (c_g, rep_gamma) from
+    ``fold_rmsnorm``.  Equals ``fused_kv_proj_grouped(rms_norm(x) * gamma, ...)`` up to
+    rounding (the normalised x is never rounded to 16 bit).
+    """
+    if not 1 <= len(specs) <= N.BD_MAX_GROUP:
+        raise ValueError(f"between 1 and {N.BD_MAX_GROUP} projections per launch")
+    x = _rowmajor(x)
+    probs = (N.KvProblem * len(specs))()
+    gam = (ctypes.c_void_p * len(specs))()
+    results = []
+    for i, (c, rg, d_h, n_heads, tag) in enumerate(specs):
+        _check(x, c, d_h, n_heads)
+        if rg.dtype != torch.float32 or rg.numel() != d_h or not rg.is_contiguous() or \
+                rg.device != x.device:
+            raise ShapeError(f"rep_gamma must be a contiguous float32 ({d_h},) tensor on x's device")
+        c = _rowmajor(c)
+        o = _out_tensor(x, d_h, n_heads, out_layout, outs[i] if outs is not None else None)
+        probs[i] = _problem(x, c, o, d_h, n_heads, tag)
+        gam[i] = rg.data_ptr()
+        results.append(o)
+    flag = torch.zeros(1, dtype=torch.int32, device=x.device) if check_finite else None
+    st = _on_device(x.device, N.load().bd_kv_proj_grouped_rmsnorm, probs, len(specs),
+                    _DTYPES[x.dtype], _MODES[mode], _LAYOUTS[out_layout], gam, float(eps),
+                    flag.data_ptr() if flag is not None else None)
+    N.check(st, "bd_kv_proj_grouped_rmsnorm")
+    _finish(flag)
+    return results
+
+
 class _HostPipeline:
     """Per-device streams, events and staging buffers of the chunked host path."""
 

@@ -41,7 +41,7 @@ from torch.nn.attention import SDPBackend, sdpa_kernel
 from .attention import select_tag
 from .decompose import Axis, Tag, bd_decompose_both, ordered_matmul
 from .errors import ShapeError
-from .kv_proj import fused_kv_proj_grouped
+from .kv_proj import fold_rmsnorm, fused_kv_proj_grouped, fused_rmsnorm_kv_proj_grouped
 
 
 # attention-core backends, in preference order (cuDNN first: it supports the MLA head
@@ -103,10 +103,17 @@ class BDMLAWeights:
     qk_candidate_residuals: tuple[float, float]
     vo_candidate_residuals: tuple[float, float]
     n_heads: int            # heads held (== cfg.n_heads unless head-sharded)
+    # kv_a_layernorm folded into the coefficients for the fused-norm projection:
+    # (c_qk_g, c_vo_g, qk_rep_gamma, vo_rep_gamma) — see kv_proj.fold_rmsnorm
+    norm_fold: tuple | None = None
 
     def to(self, device=None, dtype=None) -> "BDMLAWeights":
         f = {k: getattr(self, k).to(device=device, dtype=dtype)
              for k in ("w_q", "w_kva", "kva_norm", "c_qk", "c_vo", "b_vo")}
+        if self.norm_fold is not None:
+            cq, cv, gq, gv = self.norm_fold
+            f["norm_fold"] = (cq.to(device=device, dtype=dtype), cv.to(device=device, dtype=dtype),
+                              gq.to(device=device), gv.to(device=device))
         return replace(self, **f)
 
     @property
@@ -162,10 +169,21 @@ def mla_prepare(w: MLAWeights, *, force_first: bool = False) -> BDMLAWeights:
     dev, dt = w.w_q.device, w.w_q.dtype
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
     assert c_qk.shape == (r - nope, H * nope) and b_vo.shape == (H * dv, cfg.hidden)
-    return BDMLAWeights(cfg=cfg, w_q=t(wq_bd), w_kva=w.w_kva, kva_norm=w.kva_norm, c_qk=t(c_qk),
-                        c_vo=t(c_vo), b_vo=t(b_vo), qk_tag=qk_tag, vo_tag=vo_tag,
-                        qk_candidate_residuals=qk_means, vo_candidate_residuals=vo_means,
-                        n_heads=H)
+    return mla_fold_norm(BDMLAWeights(
+        cfg=cfg, w_q=t(wq_bd), w_kva=w.w_kva, kva_norm=w.kva_norm, c_qk=t(c_qk), c_vo=t(c_vo),
+        b_vo=t(b_vo), qk_tag=qk_tag, vo_tag=vo_tag, qk_candidate_residuals=qk_means,
+        vo_candidate_residuals=vo_means, n_heads=H))
+
+
+def mla_fold_norm(w: BDMLAWeights) -> BDMLAWeights:
+    """Attach kv_a_layernorm folded into the coefficients (``kv_proj.fold_rmsnorm``, in
+    float64, rounded once to the weights' dtype) for the fused-norm projection."""
+    cfg = w.cfg
+    gamma = w.kva_norm.detach().to(torch.float64)
+    cq, gq = fold_rmsnorm(w.c_qk.to(torch.float64), gamma, cfg.qk_nope, w.qk_tag)
+    cv, gv = fold_rmsnorm(w.c_vo.to(torch.float64), gamma, cfg.v_head, w.vo_tag)
+    dt = w.c_qk.dtype
+    return replace(w, norm_fold=(cq.to(dt), cv.to(dt), gq, gv))
 
 
 def shard_bd_mla(w: BDMLAWeights, world: int, rank: int) -> BDMLAWeights:
@@ -174,7 +192,11 @@ def shard_bd_mla(w: BDMLAWeights, world: int, rank: int) -> BDMLAWeights:
     cfg = w.cfg
     h0, h1 = head_range(w.n_heads, world, rank)
     qh, dn, dv = cfg.qk_head, cfg.qk_nope, cfg.v_head
-    return replace(w, w_q=w.w_q[:, h0 * qh:h1 * qh].contiguous(),
+    fold = None
+    if w.norm_fold is not None:
+        cq, cv, gq, gv = w.norm_fold
+        fold = (cq[:, h0 * dn:h1 * dn].contiguous(), cv[:, h0 * dv:h1 * dv].contiguous(), gq, gv)
+    return replace(w, norm_fold=fold, w_q=w.w_q[:, h0 * qh:h1 * qh].contiguous(),
                    c_qk=w.c_qk[:, h0 * dn:h1 * dn].contiguous(),
                    c_vo=w.c_vo[:, h0 * dv:h1 * dv].contiguous(),
                    b_vo=w.b_vo[h0 * dv:h1 * dv, :].contiguous(), n_heads=h1 - h0)
@@ -182,7 +204,7 @@ def shard_bd_mla(w: BDMLAWeights, world: int, rank: int) -> BDMLAWeights:
 
 # --------------------------------------------------------------------------- forward
 def _rms_norm(x: torch.Tensor, weight: torch.Tensor, eps: float) -> torch.Tensor:
-    xf = x.float()
+    xf = x.to(torch.promote_types(x.dtype, torch.float32))
     y = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)
     return (y * weight.float()).to(x.dtype)
 
@@ -251,14 +273,26 @@ def mla_forward(hidden: torch.Tensor, w: MLAWeights, *, causal: bool = True) -> 
 
 
 def bd_mla_forward(hidden: torch.Tensor, w: BDMLAWeights, *, causal: bool = True,
-                   group=None) -> torch.Tensor:
-    """BD MLA block: K'_nope and V' of all (local) heads in ONE launch of the BD kernel.
-    With head-sharded weights (``shard_bd_mla``) the partial outputs are summed with one
-    all_reduce over ``group``."""
+                   group=None, fuse_norm: bool = True) -> torch.Tensor:
+    """BD MLA block: K'_nope and V' of all (local) heads in ONE launch of the BD kernel,
+    with kv_a_layernorm fused into it (``fuse_norm``, when the weights carry the fold:
+    the raw latent is read once and never normalised in memory).  With head-sharded
+    weights (``shard_bd_mla``) the partial outputs are summed with one all_reduce over
+    ``group``."""
     cfg, H = w.cfg, w.n_heads
     L = hidden.shape[0]
     q_nope, q_pe = _split_q(hidden @ w.w_q, H, cfg)
-    c_kv, k_pe = _latent(hidden, w.w_kva, w.kva_norm, cfg)
+    # fused norm: exact kernel (float32/64) any shape; tensor cores need the latent row
+    # resident (d_h in {64, 128}, kv_lora - d_h <= 384 — DeepSeek-V2-Lite's 128 / 384)
+    fused = fuse_norm and w.norm_fold is not None and (
+        hidden.dtype in (torch.float32, torch.float64)
+        or (cfg.qk_nope in (64, 128) and cfg.v_head in (64, 128)
+            and cfg.kv_lora_rank - min(cfg.qk_nope, cfg.v_head) <= 384))
+    if fused:
+        kv = hidden @ w.w_kva
+        c_kv, k_pe = kv[:, :cfg.kv_lora_rank].contiguous(), kv[:, cfg.kv_lora_rank:]
+    else:
+        c_kv, k_pe = _latent(hidden, w.w_kva, w.kva_norm, cfg)
     rope = lambda t: _rope(t, cfg.rope_theta, cfg.rope_interleaved)  # noqa: E731
     # The BD kernel writes K'_nope head-major straight into the first qk_nope columns of
     # the attention key buffer [H, L, nope + rope] (row stride nope + rope) and V'
@@ -266,9 +300,16 @@ def bd_mla_forward(hidden: torch.Tensor, w: BDMLAWeights, *, causal: bool = True
     # copy of K'/V'; only the shared RoPE key part is broadcast into each head's tail.
     k_buf = torch.empty((H, L, cfg.qk_head), dtype=c_kv.dtype, device=c_kv.device)
     v_buf = torch.empty((H, L, cfg.v_head), dtype=c_kv.dtype, device=c_kv.device)
-    fused_kv_proj_grouped(c_kv, [(w.c_qk, cfg.qk_nope, H, w.qk_tag),
-                                 (w.c_vo, cfg.v_head, H, w.vo_tag)],
-                          outs=[k_buf[..., :cfg.qk_nope], v_buf], out_layout="head")
+    outs = [k_buf[..., :cfg.qk_nope], v_buf]
+    if fused:
+        cq, cv, gq, gv = w.norm_fold
+        fused_rmsnorm_kv_proj_grouped(c_kv, [(cq, gq, cfg.qk_nope, H, w.qk_tag),
+                                             (cv, gv, cfg.v_head, H, w.vo_tag)], cfg.rms_eps,
+                                      outs=outs, out_layout="head")
+    else:
+        fused_kv_proj_grouped(c_kv, [(w.c_qk, cfg.qk_nope, H, w.qk_tag),
+                                     (w.c_vo, cfg.v_head, H, w.vo_tag)],
+                              outs=outs, out_layout="head")
     k_buf[..., cfg.qk_nope:] = rope(k_pe)[None]
     q = torch.cat([q_nope.view(L, H, cfg.qk_nope), rope(q_pe).view(L, H, cfg.qk_rope)], -1)
     with sdpa_kernel(_BACKENDS):
@@ -348,12 +389,13 @@ def bd_mla_from_state_dict(state: dict, cfg: MLAConfig, prefix: str = "") -> BDM
             c_vo.shape != (cfg.kv_lora_rank - cfg.v_head, H * cfg.v_head):
         raise ShapeError(f"coefficient shapes {tuple(c_qk.shape)}, {tuple(c_vo.shape)} do not fit {cfg}")
     nan = (float("nan"), float("nan"))
-    return BDMLAWeights(cfg=cfg, w_q=g("q_proj.weight").T.contiguous(),
-                        w_kva=g("kv_a_proj_with_mqa.weight").T.contiguous(),
-                        kva_norm=g("kv_a_layernorm.weight").contiguous(), c_qk=c_qk, c_vo=c_vo,
-                        b_vo=g("o_proj.weight").T.contiguous(), qk_tag=tag("kv_b_proj.qk_tag"),
-                        vo_tag=tag("kv_b_proj.vo_tag"), qk_candidate_residuals=nan,
-                        vo_candidate_residuals=nan, n_heads=H)
+    w = BDMLAWeights(cfg=cfg, w_q=g("q_proj.weight").T.contiguous(),
+                     w_kva=g("kv_a_proj_with_mqa.weight").T.contiguous(),
+                     kva_norm=g("kv_a_layernorm.weight").contiguous(), c_qk=c_qk, c_vo=c_vo,
+                     b_vo=g("o_proj.weight").T.contiguous(), qk_tag=tag("kv_b_proj.qk_tag"),
+                     vo_tag=tag("kv_b_proj.vo_tag"), qk_candidate_residuals=nan,
+                     vo_candidate_residuals=nan, n_heads=H)
+    return mla_fold_norm(w)
 
 
 def rewrite_hf_checkpoint(state: dict, cfg: MLAConfig, *, dtype: torch.dtype | None = None,

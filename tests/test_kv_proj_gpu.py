@@ -387,3 +387,62 @@ def test_launch_parameter_cache_follows_buffers(cuda):
         bd.fused_kv_proj(bad, cs[0], d_h, n, bd.Tag.FIRST, check_finite=True)
     with pytest.raises(ValueError):
         bd.fused_kv_proj(bad, cs[0], d_h, n, bd.Tag.FIRST, check_finite=True)
+
+
+def _rmsnorm_bd_ref(x, cs, gamma, eps, d_h, n):
+    """float64 reference of the fused path on the kernel's exact inputs: the 16-bit x, the
+    folded (rounded) c_g and float32 rep_gamma — r * (x[:, mul] c_g + rep_gamma x[:, rep])."""
+    xd = x.double()
+    r = torch.rsqrt(xd.pow(2).mean(1, keepdim=True) + eps)
+    outs = []
+    for c_g, rg, tag in cs:
+        mul, rep = bd.tag_offsets(x.shape[1], d_h, tag)
+        K = c_g.shape[0]
+        rep_term = (rg.double()[None, :] * xd[:, rep:rep + d_h]).repeat(1, n)
+        outs.append(r * (xd[:, mul:mul + K] @ c_g.double() + rep_term))
+    return outs
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("L", [100, 256, 300, 8192])
+def test_fused_rmsnorm_projection(dtype, L, cuda):
+    """RMSNorm fused into the K'/V' projection (DeepSeek kv_a_layernorm + kv_b_proj):
+    against a float64 evaluation on the same (rounded) operands, and against the unfused
+    path (RMSNorm -> round to dtype -> projection).  L = 256 gives pairs a single tile of a
+    row-block (the A slots' release then waits for the norm's reads)."""
+    d, d_h, n, eps = 512, 128, 16, 1e-6
+    g = torch.Generator().manual_seed(L + 3)
+    x = (torch.randn(L, d, generator=g) * (0.5 + torch.rand(L, 1, generator=g) * 3)).to(dtype).to(cuda)
+    gamma = (0.5 + torch.rand(d, generator=g)).to(cuda)
+    ck = (torch.randn(d - d_h, n * d_h, generator=g) / 8).to(dtype).to(cuda)
+    cv = (torch.randn(d - d_h, n * d_h, generator=g) / 8).to(dtype).to(cuda)
+    folded = [bd.fold_rmsnorm(ck, gamma, d_h, bd.Tag.FIRST) + (bd.Tag.FIRST,),
+              bd.fold_rmsnorm(cv, gamma, d_h, bd.Tag.LAST) + (bd.Tag.LAST,)]
+    specs = [(cg, rg, d_h, n, t) for cg, rg, t in folded]
+    k, v = bd.fused_rmsnorm_kv_proj_grouped(x, specs, eps, check_finite=True)
+    kr, vr = _rmsnorm_bd_ref(x, folded, gamma, eps, d_h, n)
+    tol = {torch.float16: 2e-3, torch.bfloat16: 1.6e-2, torch.float32: 2e-6,
+           torch.float64: 1e-13}[dtype]
+    for got, ref in ((k, kr), (v, vr)):
+        err = float((got.double() - ref).abs().max() / ref.abs().max())
+        assert err <= tol, err
+    # the unfused composition: normalise, round to dtype, project
+    xn = (x.double() * torch.rsqrt(x.double().pow(2).mean(1, keepdim=True) + eps)
+          * gamma.double()).to(dtype)
+    ku, vu = bd.fused_kv_proj_grouped(xn, [(ck, d_h, n, bd.Tag.FIRST), (cv, d_h, n, bd.Tag.LAST)])
+    loose = {torch.float16: 8e-3, torch.bfloat16: 6e-2, torch.float32: 2e-5, torch.float64: 1e-12}[dtype]
+    for got, ref in ((k, ku), (v, vu)):
+        err = float((got.double() - ref.double()).abs().max() / ref.double().abs().max())
+        assert err <= loose, err
+    # head-major output of the same launch
+    kh, vh = bd.fused_rmsnorm_kv_proj_grouped(x, specs, eps, out_layout="head")
+    torch.testing.assert_close(kh, k.view(L, n, d_h).transpose(0, 1), rtol=0, atol=0)
+    torch.testing.assert_close(vh, v.view(L, n, d_h).transpose(0, 1), rtol=0, atol=0)
+
+
+def test_fused_rmsnorm_rejects_unsupported_shapes(cuda):
+    x = torch.randn(64, 200, device=cuda).half()
+    c = torch.randn(176, 24 * 5, device=cuda).half()
+    cg, rg = bd.fold_rmsnorm(c, torch.ones(200, device=cuda), 24, bd.Tag.FIRST)
+    with pytest.raises(bd.ShapeError):
+        bd.fused_rmsnorm_kv_proj_grouped(x, [(cg, rg, 24, 5, bd.Tag.FIRST)], 1e-6)
