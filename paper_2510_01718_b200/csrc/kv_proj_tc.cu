@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // shared memory.  Then out = r * (sum_k x c_g + gamma_rep x_rep) is evaluated as
           // (r * acc) + fp16(r * gamma_rep * x_rep): the rep registers are rescaled here.
           norm_pending = false;
-          float ss = 0.f;
+          float ssv[4] = {0.f, 0.f, 0.f, 0.f};  // independent chains
           const int nkb = P.num_kb;
           for (int kb = static_cast<int>(half) * 3; kb < nkb && kb < static_cast<int>(half) * 3 + 3;
                ++kb) {
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float2 f = unpack2<kBF16>(w[e]);
-                ss = fmaf(f.x, f.x, fmaf(f.y, f.y, ss));
+                ssv[e] = fmaf(f.x, f.x, fmaf(f.y, f.y, ssv[e]));
               }
             }
           }
@@ -586,11 +586,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float2 f = unpack2<kBF16>(w[e]);
-                ss = fmaf(f.x, f.x, fmaf(f.y, f.y, ss));
+                ssv[e] = fmaf(f.x, f.x, fmaf(f.y, f.y, ssv[e]));
               }
             }
           }
-          norm_part[half * BM + row_t] = ss;
+          norm_part[half * BM + row_t] = (ssv[0] + ssv[1]) + (ssv[2] + ssv[3]);
           named_bar_sync(3, 32 * EPI_WARPS);
           const float tot = norm_part[row_t] + norm_part[BM + row_t];
           rnorm = rsqrtf(tot / static_cast<float>(P.norm_d) + P.norm_eps);
