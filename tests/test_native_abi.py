@@ -120,3 +120,23 @@ def test_flop_accounting_matches_reference_bench():
     assert f"{bd.flop_ratio(512, 128):.4f}" == "1.3333"
     assert bd.flop_ratio(32, 8) == pytest.approx(32 / 24)
     assert bd.kv_flops(8192, 512, 128, 16) * 4 == 3 * 2 * 8192 * 512 * 2048
+
+
+def test_rmsnorm_and_allgather_entries_reject_bad_arguments(lib):
+    """The fused-norm and fused-all-gather entry points validate before launching."""
+    before = lib.bd_launch_count()
+    p = (N.KvProblem * 1)()
+    p[0] = N.KvProblem(1 << 20, 1 << 21, 1 << 22, 16, 16, 16, 4, 16, 8, 2, 8, 0)  # tag FIRST
+    g = (ctypes.c_void_p * 1)(1 << 23)
+    lay = N.BD_OUT_TOKEN_MAJOR
+    assert lib.bd_kv_proj_grouped_rmsnorm(p, 1, N.BD_F16, 0, lay, None, 1e-6, None, None) == N.BD_ERR_ARG
+    assert lib.bd_kv_proj_grouped_rmsnorm(p, 1, N.BD_F16, 0, lay, g, -1.0, None, None) == N.BD_ERR_ARG
+    nul = (ctypes.c_void_p * 1)(None)
+    assert lib.bd_kv_proj_grouped_rmsnorm(p, 1, N.BD_F16, 0, lay, nul, 1e-6, None, None) == N.BD_ERR_ARG
+    p[0].mul_base, p[0].rep_base = 0, 0  # slices overlap: not a FIRST / LAST partition
+    assert lib.bd_kv_proj_grouped_rmsnorm(p, 1, N.BD_F16, 0, lay, g, 1e-6, None, None) == N.BD_ERR_SHAPE
+    bufs = (ctypes.c_void_p * 2)(1 << 24, 1 << 25)
+    assert lib.bd_kv_proj_grouped_allgather(p, 1, N.BD_F16, 0, 0, 0, bufs, None, None) == N.BD_ERR_ARG
+    assert lib.bd_kv_proj_grouped_allgather(p, 1, N.BD_F16, 0, 2, 2, bufs, None, None) == N.BD_ERR_ARG
+    assert lib.bd_kv_proj_grouped_allgather(p, 1, N.BD_F16, 0, 2, 0, None, None, None) == N.BD_ERR_ARG
+    assert lib.bd_launch_count() == before
