@@ -212,9 +212,10 @@ def test_tc_head_shards_are_bit_identical(cuda):
                                        rtol=0, atol=0)
 
 
-def test_tc_strided_views(cuda):
+@pytest.mark.parametrize("L", [200, 40])  # persistent and small-L kernels
+def test_tc_strided_views(L, cuda):
     """Row-strided x/out views (e.g. a slice of a larger activation buffer) are honoured."""
-    L, d, d_h, n = 200, 256, 64, 4
+    d, d_h, n = 256, 64, 4
     g = torch.Generator().manual_seed(3)
     big = torch.randn(L, d + 64, generator=g).half().to(cuda)
     x = big[:, 32:32 + d]
