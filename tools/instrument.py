@@ -8,6 +8,10 @@ ROOT = Path(__file__).resolve().parent.parent
 import sys
 SRC = sys.argv[1] if len(sys.argv) > 1 else "paper_2510_01718_b200/csrc/kv_proj_tc.cu"
 s = (ROOT / SRC).read_text()
+# patterns apply to the persistent kernel only: set the small-L kernel and after aside
+_cut = s.find("// Small-L (\"decode\") kernel")
+tail = s[_cut:] if _cut >= 0 else ""
+s = s[:_cut] if _cut >= 0 else s
 
 
 def rep(a, b):
@@ -26,8 +30,10 @@ extern "C" int bd_debug_timeline(unsigned long long* dst) {
 }
 '''
 rep('''  const uint32_t warp = warp_id();
-  const uint32_t lane = lane_id();''', '''  const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();''', '''  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
   unsigned long long* TL = g_tl[blockIdx.x];
   if (threadIdx.x == 0) { TL[0] = GT(); TL[1] = CK(); }''')
 rep('''    for (int s = 0; s < A_SLOTS; ++s) {
@@ -47,9 +53,9 @@ rep('''  tc_fence_after();
   if (threadIdx.x == 0) TL[5] = CK();
   const uint32_t tmem_base = *tmem_slot;''')
 rep('''      griddep_wait();
-      for (int t = t_begin; t < t_end; ++t) {''', '''      griddep_wait();
+      for (int t = t_begin; t < t_end; t += t_step) {''', '''      griddep_wait();
       if (lane == 0) TL[6] = CK();
-      for (int t = t_begin; t < t_end; ++t) {''')
+      for (int t = t_begin; t < t_end; t += t_step) {''')
 for lead in ("0", "lead"):
     a = f'''            const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), {lead});'''
     if s.count(a) == 1:
@@ -88,5 +94,7 @@ rep('''        const bool reload_a = P.num_kb > A_SLOTS || key != prev_key;
         const int my_m0''')
 rep('''            mbar_wait(&a_empty[s], ((a_iter / A_SLOTS) & 1u) ^ 1u);''', '''            mbar_wait(&a_empty[s], ((a_iter / A_SLOTS) & 1u) ^ 1u);
             if (a_iter == 0 && lane == 0) TL[44] = CK();''')
+_ext = s.index('extern "C" int bd_debug_timeline')
+s = s[:_ext] + tail + "\n" + s[_ext:]
 (ROOT / "exp/kv_proj_tc_tl.cu").write_text(s)
 print("wrote exp/kv_proj_tc_tl.cu")

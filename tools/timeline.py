@@ -33,9 +33,9 @@ for _ in range(back_to_back):
     bd.fused_kv_proj_grouped(x, specs, outs=[k, v][:len(specs)])
 torch.cuda.synchronize()
 lib = _native.load()
-buf = (ctypes.c_ulonglong * (148 * 64))()
+buf = (ctypes.c_ulonglong * (148 * 96))()
 assert lib.bd_debug_timeline(buf) == 0
-tl = np.frombuffer(buf, dtype=np.uint64).reshape(148, 64).astype(np.int64)
+tl = np.frombuffer(buf, dtype=np.uint64).reshape(148, 96).astype(np.int64)
 g0 = tl[:, 0].min()
 print(f"L={L} back_to_back={back_to_back}")
 print(f"CTA start spread (ns): 0 .. {tl[:, 0].max() - g0}; end (ns): "
@@ -66,3 +66,12 @@ print("epi-end period per tile (clk) percentiles:", np.percentile(per_tile, [0, 
 order = np.argsort(endns)[-5:]
 print("slowest pairs (cta, end ns, first mma clk, period):",
       [(int(full[i]), int(endns[i]), int(first_mma[i]), int(per_tile[i])) for i in order])
+
+if tl.shape[1] > 64 and (tl[full, 64] > 0).any():
+    for base, name in ((64, "warp 2 (SMSP2)"), (80, "warp 4 (SMSP0, shared with the producer)")):
+        e = tl[full, base:base + 13]
+        rel_e = e - e[:, 11:12]  # relative to 'before tfull wait'
+        m = np.median(rel_e, axis=0).astype(int)
+        print(f"epilogue tile 3, {name}: tfull-wait-done {m[12]}, first-ld {m[1]} |",
+              "after chunk c: ", [m[2], m[4], m[6], m[8]], "| loads ready c=1..3:", [m[3], m[5], m[7]],
+              "| loop end", m[9], "| barrier done", m[10])
