@@ -35,6 +35,14 @@
 // row-block, so neither the producer nor the epilogue waits on it in steady state.
 // The add is one mixed-precision FHADD (f32 + f16/bf16) per element.  Launches use
 // programmatic dependent launch: the prologue overlaps the previous kernel's tail.
+//
+// Tile schedule: contiguous ranges per pair (A residency), or round-robin when A
+// streams (K > 384: keeps the live A/C set inside L2 — cfg3 0.74x -> 1.00x cuBLAS).
+// Variants: kCheck (non-finite flag), kRR (round-robin), kNorm (RMSNorm of x fused:
+// the epilogue sums each row's squares from the resident A slots + rep registers).
+// Also in this file: kv_proj_small_kernel, the L <= 128 (decode) path — one CTA per
+// column block, every k-block loaded at once, cta_group::1 — and the host launchers
+// with their launch-parameter cache.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
