@@ -772,14 +772,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // the main kernel.
 constexpr int SM_THREADS = 64 + 128;  // producer, MMA, 4 epilogue warps
 constexpr int SM_MAX_KB = 6;          // K <= 384
-inline size_t small_smem_bytes(int bns, int a_kb_bytes) {
-  return 1024 + SM_MAX_KB * (a_kb_bytes + (bns / 64) * B_PANEL) + 128;
+inline size_t small_smem_bytes(int bns_per_cta, int a_kb_bytes) {
+  return 1024 + SM_MAX_KB * (a_kb_bytes + (bns_per_cta / 64) * B_PANEL) + 128;
 }
 
-template <bool kBF16, bool kCheck, int BNS>
+// CGS = 2: a CTA pair (cluster of 2, cta_group::2, M = 256) covers L <= 256; each CTA
+// holds its 128 rows of A and half of the BNS-column B block, like the persistent kernel.
+template <bool kBF16, bool kCheck, int BNS, int CGS>
 __global__ void __launch_bounds__(SM_THREADS, 1)
     kv_proj_small_kernel(const __grid_constant__ TcParams prm) {
-  constexpr int PANELS = BNS / 64;
+  constexpr int PANELS = BNS / CGS / 64;
   constexpr uint32_t BS_BYTES = PANELS * B_PANEL;  // one k-block of this CTA's B
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -795,15 +797,18 @@ __global__ void __launch_bounds__(SM_THREADS, 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
 
+  const uint32_t rank = CGS == 2 ? cluster_ctarank() : 0u;  // 0 = pair leader
+
   int pi, m0, n0;
   {
-    // block -> (problem, column block); tiles_n counts BNS-wide blocks here
-    const int t = static_cast<int>(blockIdx.x);
+    // block (group) -> (problem, column block); tiles_n counts BNS-wide blocks here
+    const int t = static_cast<int>(blockIdx.x) / CGS;
     pi = 0;
     while (pi + 1 < prm.count && t >= prm.p[pi + 1].tile_start) ++pi;
     n0 = (t - prm.p[pi].tile_start) * BNS;
-    m0 = 0;
+    m0 = static_cast<int>(rank) * BM;  // this CTA's rows
   }
+  const int my_n0 = n0 + static_cast<int>(rank) * (BNS / CGS);  // this CTA's B columns
   const TcProblem& P = prm.p[pi];
   if (warp == 0 && lane == 0) {
     for (int kb = 0; kb < SM_MAX_KB; ++kb) mbar_init(&full[kb], 1);
@@ -813,51 +818,76 @@ __global__ void __launch_bounds__(SM_THREADS, 1)
     tma_prefetch_desc(&P.map_b);
   }
   if (warp == 1) {
-    tmem_alloc<1>(tmem_slot, BNS);
-    tmem_relinquish<1>();
+    tmem_alloc<CGS>(tmem_slot, BNS);
+    tmem_relinquish<CGS>();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CGS == 2)
+    cluster_sync();  // the leader's barriers exist before the peer's TMA signals them
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_launch_dependents();
 
   if (warp == 0) {
-    // ---- producer: every k-block of A and B at once (nothing to recycle)
+    // ---- producer: every k-block of A and B at once (nothing to recycle).  Pairs: both
+    // CTAs' bytes complete on the leader's barrier, armed with the pair's total.
     griddep_wait();
     if (elect_one()) {
       const uint64_t pol = policy_evict_last();  // C is shared by the row... and re-read
       for (int kb = 0; kb < P.num_kb; ++kb) {
-        mbar_arrive_expect_tx(&full[kb], a_kb + BS_BYTES);
-        tma_load_2d(sA + kb * a_kb, &P.map_a, kb * BK, m0, &full[kb], pol);
-        for (int q = 0; q < PANELS; ++q)
-          tma_load_2d(sB + kb * BS_BYTES + q * B_PANEL, &P.map_b, n0 + 64 * q, kb * BK,
-                      &full[kb], pol);
+        if constexpr (CGS == 2) {
+          if (rank == 0) mbar_arrive_expect_tx(&full[kb], CGS * (a_kb + BS_BYTES));
+          const uint32_t bar = mapa_shared(smem_u32(&full[kb]), 0);
+          tma_load_2d_pair(sA + kb * a_kb, &P.map_a, kb * BK, m0, bar, pol);
+          for (int q = 0; q < PANELS; ++q)
+            tma_load_2d_pair(sB + kb * BS_BYTES + q * B_PANEL, &P.map_b, my_n0 + 64 * q,
+                             kb * BK, bar, pol);
+        } else {
+          mbar_arrive_expect_tx(&full[kb], a_kb + BS_BYTES);
+          tma_load_2d(sA + kb * a_kb, &P.map_a, kb * BK, m0, &full[kb], pol);
+          for (int q = 0; q < PANELS; ++q)
+            tma_load_2d(sB + kb * BS_BYTES + q * B_PANEL, &P.map_b, my_n0 + 64 * q, kb * BK,
+                        &full[kb], pol);
+        }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ---- MMA: M = 128 (rows >= L are zero-filled by TMA), N = BNS, K in 16-steps
-    constexpr uint32_t idesc = make_idesc_f16(kBF16, BM, BNS, /*a_mn=*/false, /*b_mn=*/true);
-    for (int kb = 0; kb < P.num_kb; ++kb) {
-      mbar_wait(&full[kb], 0);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t a0 = smem_u32(sA + kb * a_kb);
-        const uint32_t b0 = smem_u32(sB + kb * BS_BYTES);
+    // ---- MMA (pair leader): M = 128 * CGS (rows >= L zero-filled by TMA), N = BNS
+    constexpr uint32_t idesc =
+        make_idesc_f16(kBF16, BM * CGS, BNS, /*a_mn=*/false, /*b_mn=*/true);
+    if (rank == 0) {
+      for (int kb = 0; kb < P.num_kb; ++kb) {
+        mbar_wait(&full[kb], 0);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a0 = smem_u32(sA + kb * a_kb);
+          const uint32_t b0 = smem_u32(sB + kb * BS_BYTES);
 #pragma unroll
-        for (int ks = 0; ks < BK / UK; ++ks)
-          tc_mma_f16(tmem_base, make_smem_desc(a0 + ks * (UK * 2), 16, 1024),
-                     make_smem_desc(b0 + ks * (UK * 128), B_PANEL, 1024), idesc,
-                     (kb | ks) != 0 ? 1u : 0u);
-        if (kb + 1 == P.num_kb) tc_commit(done);
+          for (int ks = 0; ks < BK / UK; ++ks) {
+            const uint64_t ad = make_smem_desc(a0 + ks * (UK * 2), 16, 1024);
+            const uint64_t bdsc = make_smem_desc(b0 + ks * (UK * 128), B_PANEL, 1024);
+            if constexpr (CGS == 2)
+              tc_mma_f16_pair(tmem_base, ad, bdsc, idesc, (kb | ks) != 0 ? 1u : 0u);
+            else
+              tc_mma_f16(tmem_base, ad, bdsc, idesc, (kb | ks) != 0 ? 1u : 0u);
+          }
+          if (kb + 1 == P.num_kb) {
+            if constexpr (CGS == 2)
+              tc_commit_pair(done, 0x3);
+            else
+              tc_commit(done);
+          }
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else {
     // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) .. (its rows), all BNS columns
     const uint32_t quad = warp & 3;
-    const int row = static_cast<int>(quad * 32 + lane);
+    const int row = m0 + static_cast<int>(quad * 32 + lane);  // this CTA's rows
     uint32_t chk = 0u;
     griddep_wait();  // the repeated slice is read from x below
     const bool live = row < P.L;
@@ -912,10 +942,13 @@ __global__ void __launch_bounds__(SM_THREADS, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CGS == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<1>(tmem_base, BNS);
+    tmem_dealloc<CGS>(tmem_base, BNS);
   }
 }
 
@@ -1057,12 +1090,21 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     cols += probs[i].N;
     max_l = probs[i].L > max_l ? probs[i].L : max_l;
   }
-  const int a_rows = static_cast<int>((max_l + 7) / 8 * 8);
+  // L <= 128: single CTAs (M = 128); 128 < L <= 256: CTA pairs (M = 256, each CTA its 128
+  // rows of A and half of the column block's B)
+  const int cgs = max_l > BM ? 2 : 1;
+  const int a_rows = cgs == 2 ? BM : static_cast<int>((max_l + 7) / 8 * 8);
   const int a_kb_bytes = a_rows * BK * 2;
-  // Column block: 64 when the CTAs that gives fit in one wave at two CTAs per SM, else
-  // 128 (C streams through as many SMs as possible in a single wave)
-  const int per_sm64 = small_smem_bytes(64, a_kb_bytes) * 2 <= 232448 ? 2 : 1;
-  const int bns = (cols + 63) / 64 <= static_cast<int64_t>(per_sm64) * sm_count() ? 64 : 128;
+  int bns;
+  if (cgs == 1) {
+    // Column block: 64 when the CTAs that gives fit in one wave at two CTAs per SM, else
+    // 128 (C streams through as many SMs as possible in a single wave)
+    const int per_sm64 = small_smem_bytes(64, a_kb_bytes) * 2 <= 232448 ? 2 : 1;
+    bns = (cols + 63) / 64 <= static_cast<int64_t>(per_sm64) * sm_count() ? 64 : 128;
+  } else {
+    // pairs: one CTA per SM (A is 96 KiB); 256-column blocks once they fill a wave
+    bns = (cols + 127) / 128 <= static_cast<int64_t>(sm_count() / 2) ? 128 : 256;
+  }
   TcParams prm{};
   prm.count = count;
   prm.flag = flag;
@@ -1099,21 +1141,28 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
   prm.total_tiles = total;
   if (total == 0) return BD_OK;
   using KernFn = void (*)(TcParams);
-  static const KernFn kerns[2][2][2] = {
-      {{kv_proj_small_kernel<false, false, 64>, kv_proj_small_kernel<false, false, 128>},
-       {kv_proj_small_kernel<false, true, 64>, kv_proj_small_kernel<false, true, 128>}},
-      {{kv_proj_small_kernel<true, false, 64>, kv_proj_small_kernel<true, false, 128>},
-       {kv_proj_small_kernel<true, true, 64>, kv_proj_small_kernel<true, true, 128>}}};
-  const int vb = bf16 ? 1 : 0, vc = flag != nullptr ? 1 : 0, vn = bns == 128 ? 1 : 0;
+  // [bf16][check][0: 1 CTA x 64, 1: 1 CTA x 128, 2: pair x 128, 3: pair x 256]
+  static const KernFn kerns[2][2][4] = {
+      {{kv_proj_small_kernel<false, false, 64, 1>, kv_proj_small_kernel<false, false, 128, 1>,
+        kv_proj_small_kernel<false, false, 128, 2>, kv_proj_small_kernel<false, false, 256, 2>},
+       {kv_proj_small_kernel<false, true, 64, 1>, kv_proj_small_kernel<false, true, 128, 1>,
+        kv_proj_small_kernel<false, true, 128, 2>, kv_proj_small_kernel<false, true, 256, 2>}},
+      {{kv_proj_small_kernel<true, false, 64, 1>, kv_proj_small_kernel<true, false, 128, 1>,
+        kv_proj_small_kernel<true, false, 128, 2>, kv_proj_small_kernel<true, false, 256, 2>},
+       {kv_proj_small_kernel<true, true, 64, 1>, kv_proj_small_kernel<true, true, 128, 1>,
+        kv_proj_small_kernel<true, true, 128, 2>, kv_proj_small_kernel<true, true, 256, 2>}}};
+  const int vb = bf16 ? 1 : 0, vc = flag != nullptr ? 1 : 0;
+  const int vn = cgs == 1 ? (bns == 128 ? 1 : 0) : (bns == 256 ? 3 : 2);
   const KernFn kern = kerns[vb][vc][vn];
-  const size_t smem = small_smem_bytes(bns, a_kb_bytes);
-  static std::atomic<bool> attr_done[2][2][2] = {};
+  const size_t smem = small_smem_bytes(bns / cgs, a_kb_bytes);
+  static std::atomic<bool> attr_done[2][2][4] = {};
   static std::mutex attr_mu;
   if (!attr_done[vb][vc][vn].load(std::memory_order_acquire)) {
     std::lock_guard<std::mutex> lock(attr_mu);
     // the largest footprint this variant can ask for
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(small_smem_bytes(bns, A_BYTES)));
+    const cudaError_t e = cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        static_cast<int>(small_smem_bytes(bns / cgs, A_BYTES)));
     if (e != cudaSuccess) {
       set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
       return BD_ERR_CUDA;
@@ -1121,15 +1170,19 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     attr_done[vb][vc][vn].store(true, std::memory_order_release);
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(total);
+  cfg.gridDim = dim3(total * cgs);
   cfg.blockDim = dim3(SM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cgs;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = cgs == 2 ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm);
   note_launch();
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -1148,10 +1201,18 @@ bool small_eligible(const Problem* probs, int count) {
     return e != nullptr && atoi(e) == 0;
   }();
   if (off) return false;
-  for (int i = 0; i < count; ++i)
-    if (probs[i].L > tc::BM || probs[i].K > tc::SM_MAX_KB * tc::BK || probs[i].world > 0 ||
+  int64_t cols = 0, max_l = 0;
+  for (int i = 0; i < count; ++i) {
+    if (probs[i].L > 2 * tc::BM || probs[i].K > tc::SM_MAX_KB * tc::BK || probs[i].world > 0 ||
         probs[i].rep_gamma != nullptr)
       return false;
+    cols += probs[i].N;
+    max_l = probs[i].L > max_l ? probs[i].L : max_l;
+  }
+  // 128 < L <= 256 (CTA pairs): only while 128-column blocks fill at most one wave of
+  // pairs — with 256-column blocks its 4-warp direct-store epilogue loses to the
+  // persistent kernel (measured: n = 128 heads, L = 256: 10.5 vs 8.1 us)
+  if (max_l > tc::BM && cols > static_cast<int64_t>(sm_count() / 2) * 128) return false;
   return true;
 }
 

@@ -344,7 +344,7 @@ def test_fused_allgather_single_device_ranks(dtype, world, cuda):
 
 
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
-@pytest.mark.parametrize("L", [1, 7, 64, 128])
+@pytest.mark.parametrize("L", [1, 7, 64, 128, 129, 200, 256])
 def test_small_l_kernel_bit_identical_to_persistent_kernel(dtype, L, cuda):
     """L <= 128 runs the small-L (decode) kernel; its rows equal, bit for bit, the same
     rows computed by the persistent kernel inside a longer batch (same FP32 tensor-core
