@@ -772,8 +772,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // the main kernel.
 constexpr int SM_THREADS = 64 + 128;  // producer, MMA, 4 epilogue warps
 constexpr int SM_MAX_KB = 6;          // K <= 384
-inline size_t small_smem_bytes(int bns_per_cta, int a_kb_bytes) {
-  return 1024 + SM_MAX_KB * (a_kb_bytes + (bns_per_cta / 64) * B_PANEL) + 128;
+constexpr uint32_t SM_STG = 4 * 2 * STG_BYTES;  // pair variant: 2 staging boxes per epilogue warp
+inline size_t small_smem_bytes(int bns_per_cta, int a_kb_bytes, bool tma_store) {
+  return 1024 + SM_MAX_KB * (a_kb_bytes + (bns_per_cta / 64) * B_PANEL) +
+         (tma_store ? SM_STG : 0) + 128;
 }
 
 // CGS = 2: a CTA pair (cluster of 2, cta_group::2, M = 256) covers L <= 256; each CTA
@@ -789,9 +791,12 @@ __global__ void __launch_bounds__(SM_THREADS, 1)
   // A k-blocks hold only the L (rounded up to 8) rows the box loads; the MMA still reads
   // 128 rows, and the rows past L land in accumulator lanes that are never stored
   const uint32_t a_kb = static_cast<uint32_t>(prm.a_kb_bytes);
+  // pairs store through smem + TMA (wide blocks); single CTAs store directly
+  constexpr bool kTma = CGS == 2;
   uint8_t* sA = smem;
   uint8_t* sB = sA + SM_MAX_KB * a_kb;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + SM_MAX_KB * BS_BYTES);
+  uint8_t* sStg = sB + SM_MAX_KB * BS_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + (kTma ? SM_STG : 0));
   uint64_t* done = full + SM_MAX_KB;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   const uint32_t warp = warp_id();
@@ -905,6 +910,65 @@ __global__ void __launch_bounds__(SM_THREADS, 1)
     }
     mbar_wait(done, 0);
     tc_fence_after();
+    if constexpr (kTma) {
+      // rows of this warp: m0 + 32 quad + [0, 32); TMA clips rows >= L and cols >= N
+      if (m0 + static_cast<int>(quad) * 32 < P.L) {
+        const uint32_t stg = smem_u32(sStg + (warp - 2) * 2 * STG_BYTES);
+#pragma unroll
+        for (int c = 0; c < BNS / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + ((quad * 32u) << 16) + c * 32, r);
+          tmem_ld_wait();
+          const int bx = c >> 1, part = c & 1;
+          const uint32_t buf = stg + static_cast<uint32_t>(bx & 1) * STG_BYTES;
+          if (part == 0 && bx >= 2) {  // the store from two boxes ago has read this buffer
+            if (lane == 0) tma_store_wait_read<1>();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const uint4 xv = xr[c * 4 + g];
+            const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+            uint32_t o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 v = add_f32_x16x2<kBF16>(__uint_as_float(r[8 * g + 2 * e]),
+                                                   __uint_as_float(r[8 * g + 2 * e + 1]), xw[e]);
+              o[e] = pack2<kBF16>(v.x, v.y);
+              if constexpr (kCheck) {
+                if (live && n0 + c * 32 + 8 * g < P.N) chk = max_abs2_nan<kBF16>(chk, o[e]);
+              }
+            }
+            const uint32_t dst = buf + lane * 128 + (((4 * part + g) ^ (lane & 7)) << 4);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(o[0]),
+                         "r"(o[1]), "r"(o[2]), "r"(o[3])
+                         : "memory");
+          }
+          if (part == 1) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            const int bcol = n0 + bx * 64;
+            if (lane == 0 && bcol < P.N) {
+              const int brow = m0 + static_cast<int>(quad) * 32;
+              if (P.head_major)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                        reinterpret_cast<uint64_t>(&P.map_out)),
+                    "r"(buf), "r"(bcol % P.out_d_h), "r"(brow), "r"(bcol / P.out_d_h)
+                    : "memory");
+              else
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                        reinterpret_cast<uint64_t>(&P.map_out)),
+                    "r"(buf), "r"(bcol), "r"(brow)
+                    : "memory");
+            }
+            if (lane == 0) tma_store_commit();  // an empty group keeps the count aligned
+          }
+        }
+        if (lane == 0) tma_store_wait_all<0>();
+      }
+    } else
 #pragma unroll
     for (int c = 0; c < BNS / 32; ++c) {
       uint32_t r[32];
@@ -1099,7 +1163,7 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
   if (cgs == 1) {
     // Column block: 64 when the CTAs that gives fit in one wave at two CTAs per SM, else
     // 128 (C streams through as many SMs as possible in a single wave)
-    const int per_sm64 = small_smem_bytes(64, a_kb_bytes) * 2 <= 232448 ? 2 : 1;
+    const int per_sm64 = small_smem_bytes(64, a_kb_bytes, false) * 2 <= 232448 ? 2 : 1;
     bns = (cols + 63) / 64 <= static_cast<int64_t>(per_sm64) * sm_count() ? 64 : 128;
   } else {
     // pairs: one CTA per SM (A is 96 KiB); 256-column blocks once they fill a wave
@@ -1117,7 +1181,12 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     const bool has_rep = q.rep_base >= 0;
     const auto* xb = static_cast<const uint16_t*>(q.x) + q.mul_base;
     if (!encode_2d(&P.map_a, xb, bf16, q.K, q.L, q.ldx, BK, a_rows, &err) ||
-        !encode_2d(&P.map_b, q.c, bf16, q.N, q.K, q.ldc, 64, BK, &err)) {
+        !encode_2d(&P.map_b, q.c, bf16, q.N, q.K, q.ldc, 64, BK, &err) ||
+        (cgs == 2 &&
+         !(q.out_layout == BD_OUT_HEAD_MAJOR
+               ? encode_3d(&P.map_out, q.out, bf16, q.d_h, q.L, q.N / q.d_h, q.ldo,
+                           q.L * q.ldo, 64, 32, &err)
+               : encode_2d(&P.map_out, q.out, bf16, q.N, q.L, q.ldo, 64, 32, &err)))) {
       set_error(err);
       return BD_ERR_CUDA;
     }
@@ -1154,7 +1223,7 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
   const int vb = bf16 ? 1 : 0, vc = flag != nullptr ? 1 : 0;
   const int vn = cgs == 1 ? (bns == 128 ? 1 : 0) : (bns == 256 ? 3 : 2);
   const KernFn kern = kerns[vb][vc][vn];
-  const size_t smem = small_smem_bytes(bns / cgs, a_kb_bytes);
+  const size_t smem = small_smem_bytes(bns / cgs, a_kb_bytes, cgs == 2);
   static std::atomic<bool> attr_done[2][2][4] = {};
   static std::mutex attr_mu;
   if (!attr_done[vb][vc][vn].load(std::memory_order_acquire)) {
@@ -1162,7 +1231,7 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     // the largest footprint this variant can ask for
     const cudaError_t e = cudaFuncSetAttribute(
         kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-        static_cast<int>(small_smem_bytes(bns / cgs, A_BYTES)));
+        static_cast<int>(small_smem_bytes(bns / cgs, A_BYTES, cgs == 2)));
     if (e != cudaSuccess) {
       set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
       return BD_ERR_CUDA;
