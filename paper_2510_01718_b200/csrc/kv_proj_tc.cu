@@ -791,8 +791,9 @@ __global__ void __launch_bounds__(SM_THREADS, 1)
   // A k-blocks hold only the L (rounded up to 8) rows the box loads; the MMA still reads
   // 128 rows, and the rows past L land in accumulator lanes that are never stored
   const uint32_t a_kb = static_cast<uint32_t>(prm.a_kb_bytes);
-  // pairs store through smem + TMA (wide blocks); single CTAs store directly
-  constexpr bool kTma = CGS == 2;
+  // 128-column blocks and pairs store through smem + TMA; 64-column blocks (two CTAs per
+  // SM, no room for staging) store directly
+  constexpr bool kTma = CGS == 2 || BNS == 128;
   uint8_t* sA = smem;
   uint8_t* sB = sA + SM_MAX_KB * a_kb;
   uint8_t* sStg = sB + SM_MAX_KB * BS_BYTES;
@@ -1169,6 +1170,7 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     // pairs: one CTA per SM (A is 96 KiB); 256-column blocks once they fill a wave
     bns = (cols + 127) / 128 <= static_cast<int64_t>(sm_count() / 2) ? 128 : 256;
   }
+  const bool tma_st = cgs == 2 || bns == 128;
   TcParams prm{};
   prm.count = count;
   prm.flag = flag;
@@ -1182,7 +1184,7 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     const auto* xb = static_cast<const uint16_t*>(q.x) + q.mul_base;
     if (!encode_2d(&P.map_a, xb, bf16, q.K, q.L, q.ldx, BK, a_rows, &err) ||
         !encode_2d(&P.map_b, q.c, bf16, q.N, q.K, q.ldc, 64, BK, &err) ||
-        (cgs == 2 &&
+        (tma_st &&
          !(q.out_layout == BD_OUT_HEAD_MAJOR
                ? encode_3d(&P.map_out, q.out, bf16, q.d_h, q.L, q.N / q.d_h, q.ldo,
                            q.L * q.ldo, 64, 32, &err)
@@ -1223,7 +1225,7 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
   const int vb = bf16 ? 1 : 0, vc = flag != nullptr ? 1 : 0;
   const int vn = cgs == 1 ? (bns == 128 ? 1 : 0) : (bns == 256 ? 3 : 2);
   const KernFn kern = kerns[vb][vc][vn];
-  const size_t smem = small_smem_bytes(bns / cgs, a_kb_bytes, cgs == 2);
+  const size_t smem = small_smem_bytes(bns / cgs, a_kb_bytes, tma_st);
   static std::atomic<bool> attr_done[2][2][4] = {};
   static std::mutex attr_mu;
   if (!attr_done[vb][vc][vn].load(std::memory_order_acquire)) {
@@ -1231,7 +1233,7 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     // the largest footprint this variant can ask for
     const cudaError_t e = cudaFuncSetAttribute(
         kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-        static_cast<int>(small_smem_bytes(bns / cgs, A_BYTES, cgs == 2)));
+        static_cast<int>(small_smem_bytes(bns / cgs, A_BYTES, tma_st)));
     if (e != cudaSuccess) {
       set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
       return BD_ERR_CUDA;
