@@ -11,6 +11,7 @@ Tolerances:
 
 import hashlib
 import json
+import os
 
 import numpy as np
 import pytest
@@ -447,3 +448,56 @@ def test_fused_rmsnorm_rejects_unsupported_shapes(cuda):
     cg, rg = bd.fold_rmsnorm(c, torch.ones(200, device=cuda), 24, bd.Tag.FIRST)
     with pytest.raises(bd.ShapeError):
         bd.fused_rmsnorm_kv_proj_grouped(x, [(cg, rg, 24, 5, bd.Tag.FIRST)], 1e-6)
+
+
+def test_tc_random_shapes_fuzz(cuda):
+    """Randomised sweep across the tensor-core kernels' dispatch space — small-L single
+    CTAs, small-L pairs, the persistent kernel with contiguous or round-robin schedules —
+    with random legal shapes, tags, dtypes, layouts, strides and grouping: every output
+    against the FP64 oracle's elementwise bound, grouped == separate bit for bit."""
+    rng = np.random.default_rng(int(os.environ.get("BD_FUZZ_SEED", "2026")))
+    for case in range(int(os.environ.get("BD_FUZZ_CASES", "60"))):
+        dtype = [torch.float16, torch.bfloat16][case % 2]
+        d_h = int(rng.choice([8, 24, 64, 128, 192]))
+        K = int(rng.choice([8, 56, 200, 384, 448, 904]))
+        d = K + d_h
+        n = int(rng.integers(1, 12))
+        L = int(rng.choice([1, 5, 64, 127, 129, 200, 256, 257, 700]))
+        layout = "head" if d_h % 64 == 0 and rng.random() < 0.4 else "token"
+        pad = int(rng.choice([0, 8, 24]))
+        g = torch.Generator().manual_seed(case)
+        big = torch.randn(L, d + pad, generator=g).to(dtype).to(cuda)
+        x = big[:, pad:pad + d] if pad else big
+        cs = [(torch.randn(K, n * d_h, generator=g) / 8).to(dtype).to(cuda) for _ in range(2)]
+        tags = [bd.Tag.FIRST, bd.Tag.LAST][:: 1 if rng.random() < 0.5 else -1]
+        specs = [(c, d_h, n, t) for c, t in zip(cs, tags)]
+        outs = bd.fused_kv_proj_grouped(x, specs, out_layout=layout, check_finite=True)
+        for (c, _, _, t), o in zip(specs, outs):
+            tok = o.transpose(0, 1).reshape(L, n * d_h) if layout == "head" else o
+            assert_tc_close(tok, x, c, d_h, n, t)
+            single = bd.fused_kv_proj(x, c, d_h, n, t, out_layout=layout, check_finite=False)
+            torch.testing.assert_close(single, o, rtol=0, atol=0)
+
+
+def test_exact_random_shapes_fuzz(cuda):
+    """The exact kernel over random shapes (any d_h, odd sizes), both tags, grouped and
+    head-major: bit-identical to the C restatement of the reference kernel."""
+    rng = np.random.default_rng(int(os.environ.get("BD_FUZZ_SEED", "7")))
+    for case in range(int(os.environ.get("BD_FUZZ_CASES", "30"))):
+        npdt = [np.float32, np.float64][case % 2]
+        d_h = int(rng.integers(1, 40))
+        d = d_h + int(rng.integers(1, 120))
+        n = int(rng.integers(1, 6))
+        L = int(rng.integers(1, 150))
+        x = rng.standard_normal((L, d)).astype(npdt)
+        cs = [(rng.standard_normal((d - d_h, n * d_h)) / 4).astype(npdt) for _ in range(2)]
+        xt = torch.from_numpy(x).to(cuda)
+        specs = [(torch.from_numpy(c).to(cuda), d_h, n, t) for c, t in zip(cs, bd.Tag)]
+        layout = "head" if case % 3 == 0 else "token"
+        outs = bd.fused_kv_proj_grouped(xt, specs, out_layout=layout)
+        for c, t, o in zip(cs, bd.Tag, outs):
+            want = O.fused_kv_proj_ref(x, c, d_h, n, t.value)
+            got = o.cpu().numpy()
+            if layout == "head":
+                got = got.transpose(1, 0, 2).reshape(L, n * d_h)
+            np.testing.assert_array_equal(got, want)
