@@ -21,10 +21,9 @@
 namespace bdk {
 namespace {
 
-constexpr int EX_BM = 64;
-constexpr int EX_BN = 64;
+// Tile T x T (T = 64, or 32 when 64-tiles would leave most SMs idle), 4 x 4 outputs per
+// thread, k-slabs of EX_BK through shared memory.
 constexpr int EX_BK = 16;
-constexpr int EX_THREADS = 256;
 
 template <typename T>
 struct ExactOps;
@@ -46,9 +45,11 @@ struct ExactGroup {
   int count;
 };
 
-template <typename T>
-__global__ void __launch_bounds__(EX_THREADS)
+template <typename T, int TILE>
+__global__ void __launch_bounds__((TILE / 4) * (TILE / 4))
     kv_proj_exact_kernel(const __grid_constant__ ExactGroup g, int* flag) {
+  constexpr int EX_BM = TILE, EX_BN = TILE, EX_THREADS = (TILE / 4) * (TILE / 4);
+  constexpr int GROUPS = TILE / 4;
   // Locate the problem and the 64x64 tile this CTA owns.
   int t = blockIdx.x;
   int pi = 0;
@@ -69,8 +70,8 @@ __global__ void __launch_bounds__(EX_THREADS)
   __shared__ T xs[EX_BK][EX_BM];  // x slab, k-major so a thread's 4 rows are contiguous
   __shared__ T cs[EX_BK][EX_BN];
 
-  const int tx = threadIdx.x % 16;  // column group
-  const int ty = threadIdx.x / 16;  // row group
+  const int tx = threadIdx.x % GROUPS;  // column group
+  const int ty = threadIdx.x / GROUPS;  // row group
   T acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -162,24 +163,38 @@ __global__ void __launch_bounds__(EX_THREADS)
 
 cudaError_t launch_exact(const Problem* probs, int count, int dtype, int* flag,
                          cudaStream_t stream) {
-  ExactGroup g{};
-  g.count = count;
-  int total = 0;
-  for (int i = 0; i < count; ++i) {
-    g.p[i] = probs[i];
-    const int64_t N = probs[i].N;
-    const int64_t tn = (N + EX_BN - 1) / EX_BN;
-    const int64_t tm = (probs[i].L + EX_BM - 1) / EX_BM;
-    g.tiles_n[i] = static_cast<int>(tn);
-    g.tile_start[i] = total;
-    total += static_cast<int>(tn * tm);
-  }
-  g.tile_start[count] = total;
+  auto tiles = [&](int t, ExactGroup& g) {
+    g = ExactGroup{};
+    g.count = count;
+    int total = 0;
+    for (int i = 0; i < count; ++i) {
+      g.p[i] = probs[i];
+      const int64_t tn = (probs[i].N + t - 1) / t;
+      const int64_t tm = (probs[i].L + t - 1) / t;
+      g.tiles_n[i] = static_cast<int>(tn);
+      g.tile_start[i] = total;
+      total += static_cast<int>(tn * tm);
+    }
+    g.tile_start[count] = total;
+    return total;
+  };
+  ExactGroup g;
+  int total = tiles(64, g);
   if (total == 0) return cudaSuccess;
+  // small problems: 32 x 32 tiles put 4x the CTAs on the SMs (the reduction itself is
+  // sequential per element, so more, smaller tiles is the only parallelism left)
+  const bool small = total < 2 * sm_count();
+  if (small) total = tiles(32, g);
   if (dtype == BD_F32) {
-    kv_proj_exact_kernel<float><<<total, EX_THREADS, 0, stream>>>(g, flag);
+    if (small)
+      kv_proj_exact_kernel<float, 32><<<total, 64, 0, stream>>>(g, flag);
+    else
+      kv_proj_exact_kernel<float, 64><<<total, 256, 0, stream>>>(g, flag);
   } else {
-    kv_proj_exact_kernel<double><<<total, EX_THREADS, 0, stream>>>(g, flag);
+    if (small)
+      kv_proj_exact_kernel<double, 32><<<total, 64, 0, stream>>>(g, flag);
+    else
+      kv_proj_exact_kernel<double, 64><<<total, 256, 0, stream>>>(g, flag);
   }
   note_launch();
   return cudaGetLastError();
