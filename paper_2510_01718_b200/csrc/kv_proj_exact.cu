@@ -78,32 +78,61 @@ __global__ void __launch_bounds__((TILE / 4) * (TILE / 4))
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
 
-  for (int64_t k0 = 0; k0 < K; k0 += EX_BK) {
-    // Stage x[m0:m0+64, mul_base+k0 : +16] and c[k0:k0+16, n0:n0+64] (zero-filled
-    // outside the problem; padded entries are never folded into acc, see kmax).
-    for (int e = threadIdx.x; e < EX_BM * EX_BK; e += EX_THREADS) {
+  // Slabs of x[m0 : m0 + T, mul_base + k0 : + EX_BK] and c[k0 : k0 + EX_BK, n0 : n0 + T]
+  // (zero-filled outside the problem; padded entries are never folded into acc, see
+  // kmax) staged through shared memory; the next slab's global loads are in flight in
+  // registers while the current one is consumed.
+  constexpr int XL = EX_BM * EX_BK / EX_THREADS;
+  constexpr int CL = EX_BN * EX_BK / EX_THREADS;
+  T xr[XL], cr[CL];
+  auto fetch = [&](int64_t k0) {
+#pragma unroll
+    for (int u = 0; u < XL; ++u) {
+      const int e = threadIdx.x + u * EX_THREADS;
       const int r = e / EX_BK, kk = e % EX_BK;
       const int64_t row = m0 + r, col = k0 + kk;
-      xs[kk][r] = (row < P.L && col < K) ? x[row * P.ldx + P.mul_base + col] : T(0);
+      xr[u] = (row < P.L && col < K) ? x[row * P.ldx + P.mul_base + col] : T(0);
     }
-    for (int e = threadIdx.x; e < EX_BN * EX_BK; e += EX_THREADS) {
+#pragma unroll
+    for (int u = 0; u < CL; ++u) {
+      const int e = threadIdx.x + u * EX_THREADS;
       const int kk = e / EX_BN, cc = e % EX_BN;
       const int64_t krow = k0 + kk, col = n0 + cc;
-      cs[kk][cc] = (krow < K && col < N) ? c[krow * P.ldc + col] : T(0);
+      cr[u] = (krow < K && col < N) ? c[krow * P.ldc + col] : T(0);
+    }
+  };
+  auto step = [&](int kk) {  // k ascending: the reference's order
+    T a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = xs[kk][ty * 4 + i];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = cs[kk][tx * 4 + j];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        acc[i][j] = ExactOps<T>::add(acc[i][j], ExactOps<T>::mul(a[i], b[j]));
+  };
+  fetch(0);
+  for (int64_t k0 = 0; k0 < K; k0 += EX_BK) {
+#pragma unroll
+    for (int u = 0; u < XL; ++u) {
+      const int e = threadIdx.x + u * EX_THREADS;
+      xs[e % EX_BK][e / EX_BK] = xr[u];
+    }
+#pragma unroll
+    for (int u = 0; u < CL; ++u) {
+      const int e = threadIdx.x + u * EX_THREADS;
+      cs[e / EX_BN][e % EX_BN] = cr[u];
     }
     __syncthreads();
+    if (k0 + EX_BK < K) fetch(k0 + EX_BK);
     const int kmax = static_cast<int>((K - k0) < EX_BK ? (K - k0) : EX_BK);
-    for (int kk = 0; kk < kmax; ++kk) {  // k ascending: the reference's order
-      T a[4], b[4];
+    if (kmax == EX_BK) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = xs[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = cs[kk][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          acc[i][j] = ExactOps<T>::add(acc[i][j], ExactOps<T>::mul(a[i], b[j]));
+      for (int kk = 0; kk < EX_BK; ++kk) step(kk);
+    } else {
+      for (int kk = 0; kk < kmax; ++kk) step(kk);
     }
     __syncthreads();
   }
