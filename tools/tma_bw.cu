@@ -39,10 +39,14 @@ __global__ void __launch_bounds__(32, 1) tma_bw_kernel(const __grid_constant__ A
   auto issue = [&](int s, int i) {
     uint8_t* dst = smem + s * STAGE_BYTES;
     mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-    const int blk = (blockIdx.x * 7 + i) % 48;  // walk an L2-resident 768 KiB..6 MiB window
+#ifndef WIN
+#define WIN 48
+#endif
+    // walk a window of WIN 8 KiB boxes of the 32 MiB (L2-resident) source
+    const int blk = static_cast<int>((blockIdx.x * 7919ull + i * 13ull) % WIN);
     if (a.mode == 0) {
-      tma_load_2d(dst, &a.map, 64 * (blk % 32), 64 * (blk % 6), &full[s], pol);
-      tma_load_2d(dst + 8192, &a.map, 64 * ((blk + 1) % 32), 64 * (blk % 6), &full[s], pol);
+      tma_load_2d(dst, &a.map, 64 * (blk % 64), 64 * ((blk / 64) % 64), &full[s], pol);
+      tma_load_2d(dst + 8192, &a.map, 64 * ((blk + 1) % 64), 64 * ((blk / 64) % 64), &full[s], pol);
     } else if (a.mode == 1) {
       tma_load_2d(dst, &a.map, 64 * (blk % 6), 128 * (blk % 32), &full[s], pol);
     } else {
