@@ -175,3 +175,38 @@ def test_bd_mla_on_rewritten_hf_checkpoint_matches_hf_attention(cuda):
     ref = _hf_forward(att, rot, hid)
     got = M.bd_mla_forward(hid.to(cuda), w).cpu()
     assert bd.max_relative_error(got, ref) <= 1e-6
+
+
+def test_fold_rmsnorm_is_the_exact_algebra():
+    """CPU: folding the RMSNorm weight into C reproduces the projection of the normalised
+    latent — r * (x[:, ~S] (diag(g) C) + g_S x[:, S]) == K'(x * r * g) in float64."""
+    rng = np.random.default_rng(5)
+    L, d_h, n = 9, 16, 3
+    d = 48
+    x = torch.from_numpy(rng.standard_normal((L, d)))
+    gamma = torch.from_numpy(0.5 + rng.random(d))
+    c = torch.from_numpy(rng.standard_normal((d - d_h, n * d_h)))
+    r = torch.rsqrt(x.pow(2).mean(1, keepdim=True) + 1e-6)
+    xn = x * r * gamma
+    for tag in bd.Tag:
+        cg, rg = bd.fold_rmsnorm(c, gamma, d_h, tag)
+        mul, rep = bd.tag_offsets(d, d_h, tag)
+        K = d - d_h
+        want = xn[:, rep:rep + d_h].repeat(1, n) + xn[:, mul:mul + K] @ c
+        got = r * (x[:, mul:mul + K] @ cg + (rg.double() * x[:, rep:rep + d_h]).repeat(1, n))
+        # rep_gamma is float32 by contract: 1e-7-level relative rounding on the rep term
+        np.testing.assert_allclose(got.numpy(), want.numpy(), rtol=1e-5, atol=1e-7)
+    assert rg.dtype == torch.float32 and cg.dtype == c.dtype
+    with pytest.raises(bd.ShapeError):
+        bd.fold_rmsnorm(c, gamma[:-1], d_h, bd.Tag.FIRST)
+
+
+def test_mla_prepare_attaches_the_norm_fold():
+    w = M.gen_random_mla(21, SMALL)
+    p = M.mla_prepare(w)
+    assert p.norm_fold is not None
+    cq, cv, gq, gv = p.norm_fold
+    assert cq.shape == p.c_qk.shape and cv.shape == p.c_vo.shape
+    assert gq.shape == (SMALL.qk_nope,) and gv.shape == (SMALL.v_head,)
+    shard = M.shard_bd_mla(p, 2, 1)
+    assert shard.norm_fold[0].shape == (p.c_qk.shape[0], p.c_qk.shape[1] // 2)
