@@ -32,17 +32,24 @@ struct Args {
   unsigned long long* clk;
 };
 
-__global__ void __launch_bounds__(64, 1) ldst_kernel(const __grid_constant__ Args a) {
+__global__ void __launch_bounds__(96, 1) ldst_kernel(const __grid_constant__ Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stg = smem + STAGES * STAGE_BYTES;  // 4 KiB store source
-  uint64_t* full = reinterpret_cast<uint64_t*>(stg + 4096);
+  uint8_t* rxbuf = stg + 4096;  // mode 2: 4 x 4 KiB receive ring
+  uint64_t* full = reinterpret_cast<uint64_t*>(rxbuf + 4 * 4096);
+  uint64_t* rx = full + STAGES;
+  uint64_t* txe = rx + 4;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&rx[s], 1);
+      mbar_init(&txe[s], 1);
+    }
     fence_mbar_init();
   }
-  __syncthreads();
+  if (a.lsu == 2) cluster_sync(); else __syncthreads();
   const uint64_t pol = policy_evict_last();
   if (warp == 0 && lane == 0) {
     auto issue = [&](int s, int i) {
@@ -61,6 +68,33 @@ __global__ void __launch_bounds__(64, 1) ldst_kernel(const __grid_constant__ Arg
     }
     for (int i = a.iters; i < a.iters + STAGES; ++i) mbar_wait(&full[i % STAGES], (i / STAGES) & 1);
     a.clk[blockIdx.x] = clock64() - t0;
+  } else if (warp == 1 && a.lsu == 2) {
+    // DSMEM traffic instead of global stores: a ring of 4 x 4 KiB buffers in the peer CTA
+    // (cluster of 2), bulk-copied smem -> peer smem, completing on the peer's rx barriers
+    if (lane == 0) {
+      const uint32_t peer = cluster_ctarank() ^ 1u;
+      for (int j = 0; j < a.stores; ++j) {
+        const int st = j % 4;
+        if (j >= 4) mbar_wait(&txe[st], ((j / 4) - 1) & 1);  // peer consumed that buffer
+        const uint32_t dst = mapa_shared(smem_u32(rxbuf + st * 4096), peer);
+        const uint32_t bar = mapa_shared(smem_u32(&rx[st]), peer);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                dst),
+            "r"(smem_u32(stg)), "r"(4096), "r"(bar)
+            : "memory");
+      }
+    }
+  } else if (warp == 2 && a.lsu == 2) {
+    if (lane == 0) {
+      const uint32_t peer = cluster_ctarank() ^ 1u;
+      for (int j = 0; j < a.stores; ++j) {
+        const int st = j % 4;
+        mbar_arrive_expect_tx(&rx[st], 4096);
+        mbar_wait(&rx[st], (j / 4) & 1);
+        mbar_arrive_remote(mapa_shared(smem_u32(&txe[st]), peer));  // buffer free again
+      }
+    }
   } else if (warp == 1 && a.lsu) {
     // the same bytes through the LSU: each warp instruction stores 512 contiguous bytes
     // (a 4 KiB box = 8 instructions), coalesced, into the same output rows
@@ -90,6 +124,7 @@ __global__ void __launch_bounds__(64, 1) ldst_kernel(const __grid_constant__ Arg
     tma_store_wait_all<0>();
     a.clk[gridDim.x + blockIdx.x] = 1;
   }
+  if (a.lsu == 2) cluster_sync();
 }
 
 int main() {
@@ -129,18 +164,24 @@ int main() {
   a.clk = clk;
   a.out = dst;
   a.iters = 3000;
-  const int smem = STAGES * STAGE_BYTES + 4096 + 2048;
+  const int smem = STAGES * STAGE_BYTES + 4096 + 4 * 4096 + 2048;
   cudaFuncSetAttribute(ldst_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int mode = 0; mode < 2; ++mode)
+  for (int mode = 0; mode < 3; ++mode)
   for (int ratio10 : {0, 3, 6, 10}) {  // store bytes per 10 load bytes
     a.lsu = mode;
     a.stores = a.iters * STAGE_BYTES / 4096 * ratio10 / 10;
-    for (int rep = 0; rep < 2; ++rep) ldst_kernel<<<sms, 64, smem>>>(a);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(sms / 2 * 2); cfg.blockDim = dim3(96); cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = mode == 2 ? 2 : 1; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    for (int rep = 0; rep < 2; ++rep) cudaLaunchKernelEx(&cfg, ldst_kernel, a);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    ldst_kernel<<<sms, 64, smem>>>(a);
+    cudaLaunchKernelEx(&cfg, ldst_kernel, a);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
@@ -151,7 +192,7 @@ int main() {
     for (auto v : h) mean += double(v) / sms;
     const double lb = double(a.iters) * STAGE_BYTES, sb = double(a.stores) * 4096;
     printf("%s store:load %.1f  loads %.1f B/clk/SM (%.2f TB/s)  total %.2f TB/s  kernel %.3f ms  (%s)\n",
-           mode ? "LSU" : "TMA", ratio10 / 10.0, lb / mean, lb * sms / (ms * 1e-3) / 1e12,
+           mode == 2 ? "DSMEM" : (mode ? "LSU" : "TMA"), ratio10 / 10.0, lb / mean, lb * sms / (ms * 1e-3) / 1e12,
            (lb + sb) * sms / (ms * 1e-3) / 1e12, ms, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
