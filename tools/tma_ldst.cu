@@ -95,7 +95,21 @@ __global__ void __launch_bounds__(96, 1) ldst_kernel(const __grid_constant__ Arg
         mbar_arrive_remote(mapa_shared(smem_u32(&txe[st]), peer));  // buffer free again
       }
     }
-  } else if (warp == 1 && a.lsu) {
+  } else if (warp == 1 && a.lsu == 3) {
+    // 1-D bulk stores of 4 KiB CONTIGUOUS bytes (vs 32 rows x 128 B boxes 8 KiB apart)
+    if (lane == 0) {
+      char* out = a.out + static_cast<size_t>(blockIdx.x) * 512 * 8192;
+      for (int j = 0; j < a.stores; ++j) {
+        const size_t off = static_cast<size_t>(j % (STORE_ROWBLK * 64)) * 4096;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + off),
+                     "r"(smem_u32(stg)), "r"(4096)
+                     : "memory");
+        tma_store_commit();
+        asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory");
+      }
+      tma_store_wait_all<0>();
+    }
+  } else if (warp == 1 && a.lsu == 1) {
     // the same bytes through the LSU: each warp instruction stores 512 contiguous bytes
     // (a 4 KiB box = 8 instructions), coalesced, into the same output rows
     uint4 v = make_uint4(lane, 1, 2, 3);
@@ -166,7 +180,7 @@ int main() {
   a.iters = 3000;
   const int smem = STAGES * STAGE_BYTES + 4096 + 4 * 4096 + 2048;
   cudaFuncSetAttribute(ldst_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int mode = 0; mode < 3; ++mode)
+  for (int mode = 0; mode < 4; ++mode)
   for (int ratio10 : {0, 3, 6, 10}) {  // store bytes per 10 load bytes
     a.lsu = mode;
     a.stores = a.iters * STAGE_BYTES / 4096 * ratio10 / 10;
@@ -192,7 +206,7 @@ int main() {
     for (auto v : h) mean += double(v) / sms;
     const double lb = double(a.iters) * STAGE_BYTES, sb = double(a.stores) * 4096;
     printf("%s store:load %.1f  loads %.1f B/clk/SM (%.2f TB/s)  total %.2f TB/s  kernel %.3f ms  (%s)\n",
-           mode == 2 ? "DSMEM" : (mode ? "LSU" : "TMA"), ratio10 / 10.0, lb / mean, lb * sms / (ms * 1e-3) / 1e12,
+           mode == 3 ? "BULK1D" : mode == 2 ? "DSMEM" : (mode ? "LSU" : "TMA"), ratio10 / 10.0, lb / mean, lb * sms / (ms * 1e-3) / 1e12,
            (lb + sb) * sms / (ms * 1e-3) / 1e12, ms, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
