@@ -263,7 +263,7 @@ def run_ours(args, rank, world, local):
         j = i % R
         bd.fused_kv_proj_grouped(xs[j], [(cks[j], d_h, n, bd.Tag.FIRST),
                                          (cvs[j], d_h, n, bd.Tag.LAST)],
-                                 outs=[kos[j], vos[j]])
+                                 outs=[kos[j], vos[j]], check_finite=False)
 
     def dense_step(i):
         j = i % R

@@ -197,11 +197,14 @@ def mha_forward(x: torch.Tensor, w: MHAWeights, *, causal: bool = False) -> torc
 
 
 def bda_forward(x: torch.Tensor, w: BDAWeights, *, causal: bool = False,
-                check_finite: bool = False) -> torch.Tensor:
+                check_finite: bool = True) -> torch.Tensor:
     """BD attention forward; output matches ``mha_forward`` (ref attention.py:298-307).
 
     K' and V' come from ONE launch of the BD kernel (two problems, each with its own
-    tag) instead of the reference's two ``fused_kv_proj`` calls.
+    tag) instead of the reference's two ``fused_kv_proj`` calls.  Like the reference,
+    whose every ``Tensor2D`` result is finite-checked (tensor.py:112-113), a non-finite
+    K', V' or output raises ``ValueError``; ``check_finite=False`` is the unchecked,
+    sync-free (CUDA-graph capturable) fast path.
     """
     _check_input(x, w.d, w.precision)
     q = _proj(x, w.b_qk)
@@ -213,9 +216,13 @@ def bda_forward(x: torch.Tensor, w: BDAWeights, *, causal: bool = False,
         qh = q.view(L, H, w.d_h).transpose(0, 1)[None]
         o = F.scaled_dot_product_attention(qh, kh[None], vh[None], is_causal=causal,
                                            scale=1.0 / math.sqrt(w.d_h))
-        return _proj(o[0].transpose(0, 1).reshape(L, H * w.d_h), w.b_vo)
-    k, v = fused_kv_proj_grouped(x, specs, check_finite=check_finite)
-    return _proj(_attend(q, k, v, w.n_heads, w.d_h, causal), w.b_vo)
+        out = _proj(o[0].transpose(0, 1).reshape(L, H * w.d_h), w.b_vo)
+    else:
+        k, v = fused_kv_proj_grouped(x, specs, check_finite=check_finite)
+        out = _proj(_attend(q, k, v, w.n_heads, w.d_h, causal), w.b_vo)
+    if check_finite and not bool(torch.isfinite(out).all()):
+        raise ValueError("operation produced non-finite values")
+    return out
 
 
 def attention_scores(x: torch.Tensor, w: MHAWeights | BDAWeights, head: int) -> torch.Tensor:

@@ -197,20 +197,34 @@ int validate_matmul(const void* a, int64_t lda, const void* b, int64_t ldb, cons
   return BD_OK;
 }
 
-// Per-thread device staging for the synchronous host entry point.
+// Per-thread device staging for the synchronous host entry point, one set per device
+// (buffers and stream belong to the device that was current when they were created).
 struct HostStaging {
   void* buf = nullptr;
   size_t cap = 0;
   int* flag = nullptr;
   cudaStream_t stream = nullptr;
-  ~HostStaging() {
-    // Process teardown may already have destroyed the context; ignore errors.
-    if (buf) cudaFree(buf);
-    if (flag) cudaFree(flag);
-    if (stream) cudaStreamDestroy(stream);
+  int device = -1;
+  void release() {
+    if (device >= 0) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(device);
+      if (buf) cudaFree(buf);
+      if (flag) cudaFree(flag);
+      if (stream) cudaStreamDestroy(stream);
+      cudaSetDevice(cur);
+    }
+    buf = nullptr;
+    cap = 0;
+    flag = nullptr;
+    stream = nullptr;
+    device = -1;
   }
+  // Process teardown may already have destroyed the context; errors are ignored.
+  ~HostStaging() { release(); }
 };
-thread_local HostStaging g_staging;
+thread_local HostStaging g_staging[4];  // a few devices per thread; more rotate through
 
 size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -219,11 +233,15 @@ size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 void set_error(const std::string& msg) { g_last_error = msg; }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-int sm_count() {
-  static std::atomic<int> cached[64] = {};  // per device ordinal, 0 = not queried yet
+int device_slot() {
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) dev = 0;
+  return dev >= 0 && dev < kMaxDevices ? dev : 0;
+}
+
+int sm_count() {
+  static std::atomic<int> cached[kMaxDevices] = {};  // per device ordinal, 0 = not queried yet
+  const int dev = device_slot();
   int n = cached[dev].load(std::memory_order_relaxed);
   if (n == 0) {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -299,9 +317,19 @@ int bd_kv_proj_host(const void* x, const void* c, void* out, int64_t L, int64_t 
   const size_t bx = round_up(static_cast<size_t>(L * d) * es, 256);
   const size_t bc = round_up(static_cast<size_t>(K * N) * es, 256);
   const size_t bo = round_up(static_cast<size_t>(L * N) * es, 256);
-  HostStaging& s = g_staging;
-  cudaError_t e = cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(BD_ERR_CUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+  HostStaging* sp = nullptr;
+  for (auto& st : g_staging)
+    if (st.device == dev) sp = &st;
+  if (sp == nullptr) {
+    sp = &g_staging[dev % 4];
+    sp->release();  // another device's set: never reuse its buffers or stream here
+  }
+  HostStaging& s = *sp;
   if (s.stream == nullptr) {
+    s.device = dev;
     e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&s.flag, sizeof(int));
     if (e != cudaSuccess) return fail(BD_ERR_CUDA, std::string("staging init: ") + cudaGetErrorString(e));

@@ -52,4 +52,9 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
 // SM count of the current device (cached).
 int sm_count();
 
+// Per-device state (function attributes, staging) is kept in arrays of this many slots,
+// indexed by device_slot(): the current device ordinal (clamped).
+constexpr int kMaxDevices = 64;
+int device_slot();
+
 }  // namespace bdk

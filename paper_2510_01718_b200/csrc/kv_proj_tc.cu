@@ -495,13 +495,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tma_load_2d(sRep + b * REP_BOX, &P.map_rep, 64 * b, m0 + static_cast<int>(rank) * BM,
                     rfull, policy_evict_last());
     };
+    // leader only: the first tile at or after t (in this pair's sequence) that belongs to
+    // a rep_fast problem and to a row-block other than `key` — the next tile whose rep
+    // tile the epilogue will wait for.  Non-fast row-blocks in between (a grouped launch
+    // may mix d_h) are skipped: nothing waits on rfull for them.
+    auto issue_next_rep = [&](int t, int key) {
+      for (; t < t_end; t += t_step) {
+        int pi, m0, n0;
+        decode_tile(prm, t, pi, m0, n0);
+        if (prm.p[pi].rep_fast && blk_key(pi, m0) != key) {
+          issue_rep(t);
+          return;
+        }
+      }
+    };
     if (leader && t_begin < t_end) {
       int pi, m0, n0;
       decode_tile(prm, t_begin, pi, m0, n0);
       const int fast0 = prm.p[pi].rep_fast;
       asm volatile("" ::"r"(fast0));
       griddep_wait();
-      if (fast0) issue_rep(t_begin);
+      issue_next_rep(t_begin, -1);
     }
     if (prm.world > 0 && lane == 0) {
       // peer tensor maps were copied to global memory before the launch: order those
@@ -547,16 +561,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                                     ((ch ^ (row_t & 7)) << 4));
         }
         named_bar_sync(2, 32 * EPI_WARPS);  // every epilogue thread holds its rep values
-        if (leader) {
-          for (int tn = t + t_step; tn < t_end; tn += t_step) {  // next row-block's rep
-            int npi, nm0, nn0;
-            decode_tile(prm, tn, npi, nm0, nn0);
-            if (blk_key(npi, nm0) != key) {
-              if (prm.p[npi].rep_fast) issue_rep(tn);
-              break;
-            }
-          }
-        }
+        if (leader) issue_next_rep(t + t_step, key);  // the next fast row-block's rep
       }
       const int acc = it % NUM_ACC;
       const uint32_t acc_phase = (it / NUM_ACC) & 1;
@@ -601,7 +606,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           norm_part[half * BM + row_t] = (ssv[0] + ssv[1]) + (ssv[2] + ssv[3]);
           named_bar_sync(3, 32 * EPI_WARPS);
           const float tot = norm_part[row_t] + norm_part[BM + row_t];
-          rnorm = rsqrtf(tot / static_cast<float>(P.norm_d) + P.norm_eps);
+          // rows past L are TMA zero-fill: with eps == 0 their rsqrt would be inf and
+          // 0 * inf a NaN that trips the non-finite check — they are never stored, use 0
+          rnorm = my_m0 + row_t < P.L ? rsqrtf(tot / static_cast<float>(P.norm_d) + P.norm_eps)
+                                      : 0.f;
           named_bar_sync(3, 32 * EPI_WARPS);  // everyone read the A slots and the partials
           if (leader)
             for (int kb = 0; kb < nkb; ++kb)
@@ -1226,9 +1234,12 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
   const int vn = cgs == 1 ? (bns == 128 ? 1 : 0) : (bns == 256 ? 3 : 2);
   const KernFn kern = kerns[vb][vc][vn];
   const size_t smem = small_smem_bytes(bns / cgs, a_kb_bytes, tma_st);
-  static std::atomic<bool> attr_done[2][2][4] = {};
+  // the attribute belongs to the function in the CURRENT device's context: set it once
+  // per device ordinal
+  static std::atomic<bool> attr_done[kMaxDevices][2][2][4] = {};
   static std::mutex attr_mu;
-  if (!attr_done[vb][vc][vn].load(std::memory_order_acquire)) {
+  const int dv = device_slot();
+  if (!attr_done[dv][vb][vc][vn].load(std::memory_order_acquire)) {
     std::lock_guard<std::mutex> lock(attr_mu);
     // the largest footprint this variant can ask for
     const cudaError_t e = cudaFuncSetAttribute(
@@ -1238,7 +1249,7 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
       set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
       return BD_ERR_CUDA;
     }
-    attr_done[vb][vc][vn].store(true, std::memory_order_release);
+    attr_done[dv][vb][vc][vn].store(true, std::memory_order_release);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(total * cgs);
@@ -1308,9 +1319,11 @@ int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_
       if (st != BD_OK) return st;
       ParamEntry& e = g_param_cache[g_param_next];
       g_param_next = (g_param_next + 1) % kParamCacheSize;
-      // an evicted all-gather entry owns its device copy of the peer maps (cudaFree waits
-      // for any kernel still reading them)
-      if (e.valid && e.prm.peer_maps) cudaFree(const_cast<CUtensorMap*>(e.prm.peer_maps));
+      // An evicted all-gather entry's device copy of the peer maps is NOT freed: a CUDA
+      // graph captured on a cache hit, or another thread that copied prm before the
+      // eviction, may still launch with that pointer, and a freed-and-reused block would
+      // turn its epilogue's peer TMA stores into writes through garbage descriptors.  The
+      // blocks live for the process (count * world * 128 B per distinct buffer set).
       e.key = key;
       e.prm = prm;
       e.valid = true;
@@ -1434,9 +1447,10 @@ int launch_params(const tc::TcParams& prm, int total, bool bf16, bool check,
   const int vb = bf16 ? 1 : 0, vc = check ? 1 : 0, vr = prm.norm ? 2 : (prm.strided ? 1 : 0);
   KernFn kern = vr == 2 ? kerns_norm[vb][vc] : kerns[vb][vc][vr];
   const size_t smem = SMEM_BYTES;
-  static std::atomic<bool> attr_set[2][2][3] = {};
+  static std::atomic<bool> attr_set[kMaxDevices][2][2][3] = {};  // per device (see launch_small)
   static std::mutex attr_mu;
-  if (!attr_set[vb][vc][vr].load(std::memory_order_acquire)) {
+  const int dv = device_slot();
+  if (!attr_set[dv][vb][vc][vr].load(std::memory_order_acquire)) {
     std::lock_guard<std::mutex> lock(attr_mu);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -1444,7 +1458,7 @@ int launch_params(const tc::TcParams& prm, int total, bool bf16, bool check,
       set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
       return BD_ERR_CUDA;
     }
-    attr_set[vb][vc][vr].store(true, std::memory_order_release);
+    attr_set[dv][vb][vc][vr].store(true, std::memory_order_release);
   }
   const int units = sm_count() / cg;
   const int grid_units = total < units ? total : units;

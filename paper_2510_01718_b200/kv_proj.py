@@ -160,13 +160,18 @@ def fused_kv_proj(x: torch.Tensor, c: torch.Tensor, d_h: int, n_heads: int,
 def fused_kv_proj_grouped(x: torch.Tensor,
                           specs: Sequence[tuple[torch.Tensor, int, int, Tag]],
                           *, outs: Sequence[torch.Tensor] | None = None,
-                          check_finite: bool = False, mode: str = "auto",
+                          check_finite: bool = True, mode: str = "auto",
                           flag: torch.Tensor | None = None,
                           out_layout: str = "token") -> list[torch.Tensor]:
     """Several projections of the same x in ONE kernel launch.
 
     ``specs`` is a list of (c, d_h, n_heads, tag) — e.g. K' and V' of
     ``bda_forward`` (ref attention.py:305-306), whose tags may differ.
+
+    Like the reference (tensor.py:112-113) a non-finite result raises ``ValueError``
+    by default, which costs one synchronisation to read the kernel's flag.  Pass
+    ``check_finite=False`` for the unchecked fast path (no sync: CUDA-graph capturable),
+    or a device int32 ``flag`` the kernel ORs into, to check later yourself.
     """
     if not 1 <= len(specs) <= N.BD_MAX_GROUP:
         raise ValueError(f"between 1 and {N.BD_MAX_GROUP} projections per launch")
@@ -214,14 +219,15 @@ def fold_rmsnorm(c: torch.Tensor, gamma: torch.Tensor, d_h: int,
 def fused_rmsnorm_kv_proj_grouped(x: torch.Tensor,
                                   specs: Sequence[tuple[torch.Tensor, torch.Tensor, int, int, Tag]],
                                   eps: float, *, outs: Sequence[torch.Tensor] | None = None,
-                                  check_finite: bool = False, mode: str = "auto",
+                                  check_finite: bool = True, mode: str = "auto",
                                   out_layout: str = "token") -> list[torch.Tensor]:
     """K'/V' of the RMS-normalised latent in ONE launch, the norm fused (one read of x).
 
     ``x`` is the raw latent (e.g. DeepSeek-V2's compressed kv before kv_a_layernorm);
     ``specs`` are (c_g, rep_gamma, d_h, n_heads, tag) with (c_g, rep_gamma) from
     ``fold_rmsnorm``.  Equals ``fused_kv_proj_grouped(rms_norm(x) * gamma, ...)`` up to
-    rounding (the normalised x is never rounded to 16 bit).
+    rounding (the normalised x is never rounded to 16 bit).  ``check_finite`` as in
+    ``fused_kv_proj_grouped``.
     """
     if not 1 <= len(specs) <= N.BD_MAX_GROUP:
         raise ValueError(f"between 1 and {N.BD_MAX_GROUP} projections per launch")
@@ -294,7 +300,12 @@ def fused_kv_proj_grouped_host(x_host: torch.Tensor,
     if outs is None:
         outs = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in dev_outs]
     caller = torch.cuda.current_stream(dev)
-    pipe.h2d.wait_stream(caller)  # device buffers are free once the caller's work is
+    # one non-finite flag for every chunk, read once after the last copy-out (the
+    # reference raises on a non-finite result, tensor.py:112-113)
+    flag = pipe.buf("flag", (1,), torch.int32, dev)
+    pipe.h2d.wait_stream(caller)
+    with torch.cuda.stream(pipe.h2d):
+        flag.zero_()  # device buffers are free once the caller's work is
     step = max(1, -(-L // max(1, chunks)))
     step = -(-step // 256) * 256  # whole 256-row CTA-pair tiles per block
     done = None
@@ -304,7 +315,8 @@ def fused_kv_proj_grouped_host(x_host: torch.Tensor,
             xd[r0:r1].copy_(x_host[r0:r1], non_blocking=True)
         pipe.comp.wait_stream(pipe.h2d)
         with torch.cuda.stream(pipe.comp):
-            fused_kv_proj_grouped(xd[r0:r1], specs, outs=[o[r0:r1] for o in dev_outs], mode=mode)
+            fused_kv_proj_grouped(xd[r0:r1], specs, outs=[o[r0:r1] for o in dev_outs], mode=mode,
+                                  flag=flag)
         pipe.d2h.wait_stream(pipe.comp)
         with torch.cuda.stream(pipe.d2h):
             for o, r in zip(outs, dev_outs):
@@ -314,6 +326,8 @@ def fused_kv_proj_grouped_host(x_host: torch.Tensor,
     if done is not None:
         done.synchronize()
     caller.wait_stream(pipe.d2h)
+    if int(flag.item()) != 0:
+        raise ValueError("operation produced non-finite values")
     return list(outs)
 
 

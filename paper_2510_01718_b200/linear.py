@@ -124,8 +124,11 @@ def bd_linear_from_lowrank(layer: LowRankLayer, *, prepare_in_p64: bool = False,
 
 
 def bd_linear_forward(x: torch.Tensor, layer: BDLinearLayer, *, out: torch.Tensor | None = None,
-                      check_finite: bool = False, mode: str = "auto") -> torch.Tensor:
-    """Two-step forward h = x B; y = [h, h C] / [h C, h] (ref linear.py:101-108)."""
+                      check_finite: bool = True, mode: str = "auto") -> torch.Tensor:
+    """Two-step forward h = x B; y = [h, h C] / [h C, h] (ref linear.py:101-108).
+
+    A non-finite result raises ``ValueError`` like the reference (tensor.py:112-113);
+    ``check_finite=False`` skips the flag read (no synchronisation)."""
     if x.dim() != 2 or x.shape[1] != layer.d_in:
         raise ShapeError(f"input has {x.shape[-1]} cols, layer expects {layer.d_in}")
     if x.dtype != layer.basis.dtype or x.dtype != layer.coeff.dtype:

@@ -305,11 +305,11 @@ def bd_mla_forward(hidden: torch.Tensor, w: BDMLAWeights, *, causal: bool = True
         cq, cv, gq, gv = w.norm_fold
         fused_rmsnorm_kv_proj_grouped(c_kv, [(cq, gq, cfg.qk_nope, H, w.qk_tag),
                                              (cv, gv, cfg.v_head, H, w.vo_tag)], cfg.rms_eps,
-                                      outs=outs, out_layout="head")
+                                      outs=outs, out_layout="head", check_finite=False)
     else:
         fused_kv_proj_grouped(c_kv, [(w.c_qk, cfg.qk_nope, H, w.qk_tag),
                                      (w.c_vo, cfg.v_head, H, w.vo_tag)],
-                              outs=outs, out_layout="head")
+                              outs=outs, out_layout="head", check_finite=False)
     k_buf[..., cfg.qk_nope:] = rope(k_pe)[None]
     q = torch.cat([q_nope.view(L, H, cfg.qk_nope), rope(q_pe).view(L, H, cfg.qk_rope)], -1)
     with sdpa_kernel(_BACKENDS):

@@ -149,8 +149,11 @@ class ErrorReport:
     precision: torch.dtype
 
 
-def _np64(t: torch.Tensor) -> np.ndarray:
-    return np.ascontiguousarray(t.detach().to("cpu", torch.float64).numpy())
+def _np(t: torch.Tensor) -> np.ndarray:
+    """Host array in the tensor's own precision: the reference forms the per-head
+    products in the layer precision (verify.py:102-124, ``_fast_matmul``) and widens
+    only the results to 64 bit (:136-137)."""
+    return np.ascontiguousarray(t.detach().to("cpu").numpy())
 
 
 def reconstruction_error_report(w: MHAWeights, prepared: BDAWeights,
@@ -160,9 +163,9 @@ def reconstruction_error_report(w: MHAWeights, prepared: BDAWeights,
     if (w.d, w.n_heads, w.d_h) != (prepared.d, prepared.n_heads, prepared.d_h):
         raise ValueError("weight geometries differ between model and prepared form")
     d_h = w.d_h
-    wq, wk, wv, wo = (_np64(t) for t in (w.w_q, w.w_k, w.w_v, w.w_o))
-    bqk, cqk, cvo, bvo = (_np64(t) for t in (prepared.b_qk, prepared.c_qk, prepared.c_vo,
-                                              prepared.b_vo))
+    wq, wk, wv, wo = (_np(t) for t in (w.w_q, w.w_k, w.w_v, w.w_o))
+    bqk, cqk, cvo, bvo = (_np(t) for t in (prepared.b_qk, prepared.c_qk, prepared.c_vo,
+                                            prepared.b_vo))
     per_head, max_rel = [], 0.0
     for i in range(w.n_heads):
         lo, hi = i * d_h, (i + 1) * d_h
@@ -178,7 +181,8 @@ def reconstruction_error_report(w: MHAWeights, prepared: BDAWeights,
             rebuilt = blas_matmul(coeff, basis)
             parts = [basis, rebuilt] if prepared.vo_tag is Tag.FIRST else [rebuilt, basis]
             recon = np.concatenate(parts, axis=0)
-        diff = recon - ref
+        ref = ref.astype(np.float64)
+        diff = recon.astype(np.float64) - ref
         mse = float(np.mean(diff * diff))
         power = float(np.mean(ref * ref))
         nmse = mse / power if power > 0.0 else (0.0 if mse == 0.0 else math.inf)

@@ -20,6 +20,8 @@ It imports bdattn 0.1.0 from /root/reference/pkg/src without writing into it
                    small seeded models, so a port of the prep can be checked bit-exactly
                    for the selected basis S.
   linear_small.npz bd_linear_forward / lowrank_forward on small seeded layers.
+  recon_report.json reconstruction_error_report (verify.py:127-155) of bda_prepare on
+                   small seeded models, both targets, P64 and P32 (floats as repr).
 
 The GPU box never reads /root/reference; tests read only these committed files.
 """
@@ -163,6 +165,27 @@ def linear_small() -> None:
     print(f"linear_small: {len(meta)} cases")
 
 
+def recon_report() -> None:
+    from bdattn.verify import Target, reconstruction_error_report
+    cases = []
+    for seed in range(4):
+        for (d, d_h, n) in ((64, 16, 4), (24, 4, 5)):
+            for precision, p64 in ((Precision.P64, False), (Precision.P32, True)):
+                w = bd.gen_random_mha(Rng(100 + seed), d, d_h, n, precision)
+                p = bd.bda_prepare(w, prepare_in_p64=p64)
+                for target in (Target.QK, Target.VO):
+                    r = reconstruction_error_report(w, p, target)
+                    cases.append({
+                        "seed": 100 + seed, "d": d, "d_h": d_h, "n_heads": n,
+                        "precision": precision.value, "prepare_in_p64": p64,
+                        "target": target.value, "mse": repr(r.mse), "nmse": repr(r.nmse),
+                        "max_rel": repr(r.max_rel),
+                        "per_head": [[repr(a), repr(b)] for a, b in r.per_head],
+                    })
+    (OUT / "recon_report.json").write_text(json.dumps(cases, indent=0) + "\n")
+    print(f"recon_report: {len(cases)} cases")
+
+
 def bundle() -> None:
     """A prepared bundle written by the reference's own tensorio (`bdattn prepare`
     output format): MHA and BDA manifests + BDT1 files for a small seeded model."""
@@ -178,6 +201,7 @@ def bundle() -> None:
 
 if __name__ == "__main__":
     import sys as _sys
-    todo = _sys.argv[1:] or ["fused_small", "cfg1", "prep_tags", "linear_small", "bundle"]
+    todo = _sys.argv[1:] or ["fused_small", "cfg1", "prep_tags", "linear_small", "recon_report",
+                             "bundle"]
     for name in todo:
         globals()[name]()

@@ -461,21 +461,26 @@ def test_tc_random_shapes_fuzz(cuda):
         d_h = int(rng.choice([8, 24, 64, 128, 192]))
         K = int(rng.choice([8, 56, 200, 384, 448, 904]))
         d = K + d_h
+        # the second problem may use another head width (same x, so K differs too);
+        # head-major output needs d_h % 64 == 0 for every problem of the launch
+        d_h2 = d_h if rng.random() < 0.5 else int(rng.choice([8, 24, 64, 128]))
+        d_h2 = d_h2 if d_h2 < d else d_h
         n = int(rng.integers(1, 12))
         L = int(rng.choice([1, 5, 64, 127, 129, 200, 256, 257, 700]))
-        layout = "head" if d_h % 64 == 0 and rng.random() < 0.4 else "token"
+        layout = "head" if d_h % 64 == 0 and d_h2 % 64 == 0 and rng.random() < 0.4 else "token"
         pad = int(rng.choice([0, 8, 24]))
         g = torch.Generator().manual_seed(case)
         big = torch.randn(L, d + pad, generator=g).to(dtype).to(cuda)
         x = big[:, pad:pad + d] if pad else big
-        cs = [(torch.randn(K, n * d_h, generator=g) / 8).to(dtype).to(cuda) for _ in range(2)]
+        dhs = [d_h, d_h2]
+        cs = [(torch.randn(d - dh, n * dh, generator=g) / 8).to(dtype).to(cuda) for dh in dhs]
         tags = [bd.Tag.FIRST, bd.Tag.LAST][:: 1 if rng.random() < 0.5 else -1]
-        specs = [(c, d_h, n, t) for c, t in zip(cs, tags)]
+        specs = [(c, dh, n, t) for c, dh, t in zip(cs, dhs, tags)]
         outs = bd.fused_kv_proj_grouped(x, specs, out_layout=layout, check_finite=True)
-        for (c, _, _, t), o in zip(specs, outs):
-            tok = o.transpose(0, 1).reshape(L, n * d_h) if layout == "head" else o
-            assert_tc_close(tok, x, c, d_h, n, t)
-            single = bd.fused_kv_proj(x, c, d_h, n, t, out_layout=layout, check_finite=False)
+        for (c, dh, _, t), o in zip(specs, outs):
+            tok = o.transpose(0, 1).reshape(L, n * dh) if layout == "head" else o
+            assert_tc_close(tok, x, c, dh, n, t)
+            single = bd.fused_kv_proj(x, c, dh, n, t, out_layout=layout, check_finite=False)
             torch.testing.assert_close(single, o, rtol=0, atol=0)
 
 
@@ -501,3 +506,54 @@ def test_exact_random_shapes_fuzz(cuda):
             if layout == "head":
                 got = got.transpose(1, 0, 2).reshape(L, n * d_h)
             np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("order", [(96, 128), (128, 96), (8, 64, 128, 24)])
+def test_grouped_mixed_d_h_rep_staging_order(order, cuda):
+    """Grouped launch where a problem whose rep tile is NOT staged (d_h not in {64, 128})
+    precedes one whose rep tile is (the look-ahead that stages the next
+    row-block's rep must skip non-staged row-blocks, or the pair whose range crosses
+    into the staged problem waits forever).  L > 256 so pairs span both problems."""
+    L, d = 700, 480
+    g = torch.Generator().manual_seed(sum(order))
+    x = torch.randn(L, d, generator=g).half().to(cuda)
+    specs = []
+    for i, d_h in enumerate(order):
+        n = max(1, 512 // d_h)
+        c = (torch.randn(d - d_h, n * d_h, generator=g) / 8).half().to(cuda)
+        specs.append((c, d_h, n, [bd.Tag.FIRST, bd.Tag.LAST][i % 2]))
+    outs = bd.fused_kv_proj_grouped(x, specs, check_finite=True)
+    torch.cuda.synchronize()
+    for o, (c, d_h, n, t) in zip(outs, specs):
+        assert_tc_close(o, x, c, d_h, n, t)
+        torch.testing.assert_close(o, bd.fused_kv_proj(x, c, d_h, n, t), rtol=0, atol=0)
+
+
+def test_fused_rmsnorm_eps_zero_ragged_l_is_finite(cuda):
+    """eps = 0 with L not a multiple of 256: rows past L (TMA zero-fill) must not trip
+    the non-finite check (rsqrt(0) * 0 = NaN in padding rows)."""
+    L, d, d_h, n = 300, 512, 128, 16
+    g = torch.Generator().manual_seed(17)
+    x = torch.randn(L, d, generator=g).half().to(cuda)
+    gamma = (0.5 + torch.rand(d, generator=g)).to(cuda)
+    ck = (torch.randn(d - d_h, n * d_h, generator=g) / 8).half().to(cuda)
+    cv = (torch.randn(d - d_h, n * d_h, generator=g) / 8).half().to(cuda)
+    folded = [bd.fold_rmsnorm(ck, gamma, d_h, bd.Tag.FIRST) + (bd.Tag.FIRST,),
+              bd.fold_rmsnorm(cv, gamma, d_h, bd.Tag.LAST) + (bd.Tag.LAST,)]
+    specs = [(cg, rg, d_h, n, t) for cg, rg, t in folded]
+    k, v = bd.fused_rmsnorm_kv_proj_grouped(x, specs, 0.0, check_finite=True)
+    kr, vr = _rmsnorm_bd_ref(x, folded, gamma, 0.0, d_h, n)
+    for got, ref in ((k, kr), (v, vr)):
+        assert float((got.double() - ref).abs().max() / ref.abs().max()) <= 2e-3
+
+
+def test_check_finite_is_the_default_like_the_reference(cuda):
+    """ref tensor.py:112-113 raises on any non-finite result: the grouped call and
+    bda_forward do too unless asked not to."""
+    x = torch.randn(64, 96, device=cuda).half()
+    x[3, 50] = float("inf")
+    c = torch.randn(64, 64, device=cuda).half()
+    with pytest.raises(ValueError, match="non-finite"):
+        bd.fused_kv_proj_grouped(x, [(c, 32, 2, bd.Tag.FIRST)])
+    out = bd.fused_kv_proj_grouped(x, [(c, 32, 2, bd.Tag.FIRST)], check_finite=False)
+    assert not bool(torch.isfinite(out[0]).all())

@@ -125,3 +125,22 @@ def test_weight_carriers_validate_like_the_reference():
     with pytest.raises(bd.PrecisionError):
         bd.MHAWeights(16, 2, 4, w.w_q.float(), w.w_k, w.w_v, w.w_o)
     assert w.param_count == 4 * 16 * 8
+
+
+def test_reconstruction_error_report_matches_reference():
+    """verify.reconstruction_error_report (ref verify.py:127-155) on the reference's own
+    prepared factors: per-head MSE/NMSE and max-rel, both targets, P64 and P32 prep."""
+    from paper_2510_01718_b200.verify import Target, reconstruction_error_report
+    cases = json.loads((GOLDEN / "recon_report.json").read_text())
+    assert len(cases) == 32
+    for c in cases:
+        w = bd.gen_random_mha(bd.Rng(c["seed"]), c["d"], c["d_h"], c["n_heads"], DT[c["precision"]])
+        p = bd.bda_prepare(w, prepare_in_p64=c["prepare_in_p64"])
+        r = reconstruction_error_report(w, p, Target(c["target"]))
+        where = f"case {c['seed']} {c['d']}/{c['d_h']}/{c['n_heads']} {c['precision']} {c['target']}"
+        assert r.precision == p.precision, where
+        # same per-head products in the layer precision (platform BLAS, one thread) and
+        # the same FP64 reductions: the report reproduces the reference bit for bit
+        assert repr(r.mse) == c["mse"] and repr(r.nmse) == c["nmse"], where
+        assert repr(r.max_rel) == c["max_rel"], where
+        assert [[repr(a), repr(b)] for a, b in r.per_head] == c["per_head"], where
