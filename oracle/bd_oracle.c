@@ -40,8 +40,13 @@ typedef struct {
   int fused;
 } job_t;
 
+/* Built for AVX-512 and AVX2 (the loader picks the host's best at run time, like
+ * numba's -march=native JIT): vector width does not change any element's rounding
+ * sequence — every lane is an independent out[i, j] chain. */
+#define BD_CLONES __attribute__((target_clones("arch=x86-64-v4", "arch=x86-64-v3", "default")))
+
 #define DEFINE_BLOCKS(SUFFIX, T)                                                  \
-  static void blocks_##SUFFIX(const job_t* j) {                                   \
+  BD_CLONES static void blocks_##SUFFIX(const job_t* j) {                        \
     const T* x = (const T*)j->x;                                                  \
     const T* c = (const T*)j->c;                                                  \
     T* out = (T*)j->out;                                                          \
