@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libbd_kvproj.so"
 SOURCES = ["capi.cu", "kv_proj_exact.cu", "kv_proj_tc.cu"]
-HEADERS = ["ptx_sm100.cuh", "kv_proj_internal.h"]
+HEADERS = ["ptx_sm100.cuh", "kv_proj_internal.h", "tc_common.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

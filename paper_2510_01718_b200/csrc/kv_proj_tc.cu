@@ -59,6 +59,7 @@
 
 #include "kv_proj_internal.h"
 #include "ptx_sm100.cuh"
+#include "tc_common.cuh"
 
 namespace bdk {
 namespace tc {
@@ -90,44 +91,6 @@ constexpr size_t SMEM_BYTES = 1024 + A_SLOTS * A_BYTES + B_STAGES * B_BYTES + RE
                               EPI_WARPS * STG_BUFS * STG_BYTES + 512 + NORM_SCRATCH;
 static_assert((2 * A_SLOTS + 2 * B_STAGES + 2 * NUM_ACC + 1) * 8 + 4 <= 512, "barrier area");
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
-
-struct TcProblem {
-  CUtensorMap map_a;    // x + mul_base, dims {K, L},   box {64, 128}
-  CUtensorMap map_b;    // c,            dims {N, K},   box {64, BKB}
-  CUtensorMap map_rep;  // x + rep_base, dims {d_h, L}, box {64, 128}   (rep_fast only)
-  CUtensorMap map_out;  // out: token-major dims {N, L}, box {64, 32}; head-major dims
-                        // {d_h, L, n_heads}, box {64, 32, 1} (clips per head); SW128
-  const void* x;
-  int64_t ldx;
-  int32_t L, N, K, d_h, rep_base;
-  int32_t tiles_n, num_kb, num_kbb, tile_start;  // num_kbb: B k-blocks (BKB deep)
-  int32_t has_rep;      // 0: plain GEMM (no repeated-slice add)
-  int32_t rep_fast;     // d_h in {64, 128}: rep tile staged in smem by TMA
-  int32_t head_major;   // output layout [n_heads][L][d_h]
-  int32_t out_d_h;      // head width of the head-major output
-  void* out;            // output base and row stride (the small-L kernel stores directly)
-  int64_t ldo;
-  const float* rep_gamma;  // kNorm: RMSNorm weight of the repeated slice (d_h floats)
-  float norm_eps;          // kNorm: RMSNorm epsilon
-  int32_t norm_d;          // kNorm: columns of x's row (K + d_h) the norm averages over
-};
-
-struct TcParams {
-  TcProblem p[BD_MAX_GROUP];
-  // fused all-gather: per problem, the head-major 3-D map {d_h, L, world * n_heads} of
-  // every rank's gathered buffer (peer memory over NVLink); world == 0 otherwise
-  // [count][world] in device memory (kept out of the kernel parameters: 4 KB more of
-  // them costs ~2 us of host time per launch); null when world == 0
-  const CUtensorMap* peer_maps;
-  int32_t world;
-  int32_t head0[BD_MAX_GROUP];
-  int32_t count;
-  int32_t total_tiles;  // tiles of (BM * CG) rows x BN columns
-  int32_t a_kb_bytes;   // small-L kernel: bytes of one A k-block (rows rounded to 8 x 128 B)
-  int32_t strided;      // tiles dealt round-robin to the pairs (streaming-A problems)
-  int32_t norm;         // fused RMSNorm (kNorm variant)
-  int* flag;            // non-finite flag (kCheck instantiation only)
-};
 
 __device__ __forceinline__ void decode_tile(const TcParams& prm, int t, int& pi, int& m0,
                                             int& n0) {
@@ -187,76 +150,6 @@ __device__ __forceinline__ void cursor_next(const TcParams& prm, TileCursor& c) 
 
 // Tiles sharing (problem, pair row-block) share the A row-block and the rep tile.
 __device__ __forceinline__ int blk_key(int pi, int m0) { return (pi << 24) | (m0 / (BM * CG)); }
-
-template <bool kBF16>
-__device__ __forceinline__ uint32_t pack2(float a, float b) {
-  if constexpr (kBF16) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-  } else {
-    __half2 h = __floats2half2_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-  }
-}
-
-template <bool kBF16>
-__device__ __forceinline__ float2 unpack2(uint32_t w) {
-  if constexpr (kBF16) {
-    __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&w);
-    return __bfloat1622float2(h);
-  } else {
-    __half2 h = *reinterpret_cast<__half2*>(&w);
-    return __half22float2(h);
-  }
-}
-
-// (a + lo(h), b + hi(h)) in FP32 with the 16-bit halves of h widened exactly: the
-// mixed-precision add.f32.f16 / add.f32.bf16 (one FHADD per element on sm_100).
-template <bool kBF16>
-__device__ __forceinline__ float2 add_f32_x16x2(float a, float b, uint32_t h) {
-  float r0, r1;
-  if constexpr (kBF16)
-    asm("{ .reg .b16 lo, hi; mov.b32 {lo, hi}, %2; add.rn.f32.bf16 %0, lo, %3;"
-        " add.rn.f32.bf16 %1, hi, %4; }"
-        : "=f"(r0), "=f"(r1) : "r"(h), "f"(a), "f"(b));
-  else
-    asm("{ .reg .b16 lo, hi; mov.b32 {lo, hi}, %2; add.rn.f32.f16 %0, lo, %3;"
-        " add.rn.f32.f16 %1, hi, %4; }"
-        : "=f"(r0), "=f"(r1) : "r"(h), "f"(a), "f"(b));
-  return make_float2(r0, r1);
-}
-
-// Packed FP32 add (FADD2 on sm_100): two lanes per instruction, each rounded once.
-__device__ __forceinline__ float2 add_f32x2(float2 a, float2 b) {
-  unsigned long long av = *reinterpret_cast<unsigned long long*>(&a);
-  unsigned long long bv = *reinterpret_cast<unsigned long long*>(&b);
-  unsigned long long r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(av), "l"(bv));
-  return *reinterpret_cast<float2*>(&r);
-}
-
-// Running packed max of |h| that propagates NaN (one HMNMX2 per two outputs).
-template <bool kBF16>
-__device__ __forceinline__ uint32_t max_abs2_nan(uint32_t acc, uint32_t w) {
-  if constexpr (kBF16) {
-    __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&acc);
-    __nv_bfloat162 b = __habs2(*reinterpret_cast<__nv_bfloat162*>(&w));
-    __nv_bfloat162 m = __hmax2_nan(a, b);
-    return *reinterpret_cast<uint32_t*>(&m);
-  } else {
-    __half2 a = *reinterpret_cast<__half2*>(&acc);
-    __half2 b = __habs2(*reinterpret_cast<__half2*>(&w));
-    __half2 m = __hmax2_nan(a, b);
-    return *reinterpret_cast<uint32_t*>(&m);
-  }
-}
-
-// Either 16-bit lane of a packed max is Inf or NaN (exponent bits all ones).
-template <bool kBF16>
-__device__ __forceinline__ bool nonfinite2(uint32_t w) {
-  const uint32_t e = kBF16 ? 0x7F80u : 0x7C00u;
-  return ((w & e) == e) || (((w >> 16) & e) == e);
-}
 
 // kCheck: compute the non-finite flag (instantiated only when the caller asked for it).
 // kRR: round-robin tile schedule (streaming-A problems), else contiguous ranges.
@@ -815,12 +708,15 @@ __global__ void __launch_bounds__(SM_THREADS, 1)
 
   int pi, m0, n0;
   {
-    // block (group) -> (problem, column block); tiles_n counts BNS-wide blocks here
-    const int t = static_cast<int>(blockIdx.x) / CGS;
+    // block (group) -> (problem, column block, row block); tiles_n counts BNS-wide
+    // blocks here, row blocks are BM * CGS rows (one for L <= 128 * CGS)
+    const int tb = static_cast<int>(blockIdx.x) / CGS;
+    const int nrb = prm.small_rblocks;
+    const int t = tb / nrb;
     pi = 0;
     while (pi + 1 < prm.count && t >= prm.p[pi + 1].tile_start) ++pi;
     n0 = (t - prm.p[pi].tile_start) * BNS;
-    m0 = static_cast<int>(rank) * BM;  // this CTA's rows
+    m0 = (tb % nrb) * (BM * CGS) + static_cast<int>(rank) * BM;  // this CTA's rows
   }
   const int my_n0 = n0 + static_cast<int>(rank) * (BNS / CGS);  // this CTA's B columns
   const TcProblem& P = prm.p[pi];
@@ -830,6 +726,16 @@ __global__ void __launch_bounds__(SM_THREADS, 1)
     fence_mbar_init();
     tma_prefetch_desc(&P.map_a);
     tma_prefetch_desc(&P.map_b);
+    // This CTA's C slice into L2 before the PDL wait: L2 is the GPU's point of
+    // coherence, so a prefetch can never return stale data even if the previous kernel
+    // wrote C — it only starts the DRAM read of the weights under that kernel's tail.
+    // (x, which the previous kernel may produce, is read only after the wait.)
+    for (int kb = 0; kb < P.num_kb; ++kb)
+      for (int q = 0; q < PANELS; ++q)
+        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                         reinterpret_cast<uint64_t>(&P.map_b)),
+                     "r"(my_n0 + 64 * q), "r"(kb * BK)
+                     : "memory");
   }
   if (warp == 1) {
     tmem_alloc<CGS>(tmem_slot, BNS);
@@ -1043,7 +949,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // Row-major [rows x cols] 16-bit matrix, row stride ld elements, box {box_cols, box_rows}.
 bool encode_2d(CUtensorMap* map, const void* base, bool bf16, uint64_t cols, uint64_t rows,
                uint64_t ld, uint32_t box_cols, uint32_t box_rows, std::string* err,
-               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+               CUtensorMapSwizzle swz) {
   auto fn = encode_fn();
   if (fn == nullptr) {
     *err = "cuTensorMapEncodeTiled unavailable from the driver";
@@ -1166,6 +1072,7 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
   // L <= 128: single CTAs (M = 128); 128 < L <= 256: CTA pairs (M = 256, each CTA its 128
   // rows of A and half of the column block's B)
   const int cgs = max_l > BM ? 2 : 1;
+  const int nrb = static_cast<int>((max_l + BM * cgs - 1) / (BM * cgs));  // row blocks
   const int a_rows = cgs == 2 ? BM : static_cast<int>((max_l + 7) / 8 * 8);
   const int a_kb_bytes = a_rows * BK * 2;
   int bns;
@@ -1176,13 +1083,14 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     bns = (cols + 63) / 64 <= static_cast<int64_t>(per_sm64) * sm_count() ? 64 : 128;
   } else {
     // pairs: one CTA per SM (A is 96 KiB); 256-column blocks once they fill a wave
-    bns = (cols + 127) / 128 <= static_cast<int64_t>(sm_count() / 2) ? 128 : 256;
+    bns = (cols + 127) / 128 * nrb <= static_cast<int64_t>(sm_count() / 2) ? 128 : 256;
   }
   const bool tma_st = cgs == 2 || bns == 128;
   TcParams prm{};
   prm.count = count;
   prm.flag = flag;
   prm.a_kb_bytes = a_kb_bytes;
+  prm.small_rblocks = nrb;
   int total = 0;
   for (int i = 0; i < count; ++i) {
     const Problem& q = probs[i];
@@ -1252,7 +1160,7 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     attr_done[dv][vb][vc][vn].store(true, std::memory_order_release);
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(total * cgs);
+  cfg.gridDim = dim3(total * cgs * nrb);
   cfg.blockDim = dim3(SM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -1283,24 +1191,43 @@ bool small_eligible(const Problem* probs, int count) {
     return e != nullptr && atoi(e) == 0;
   }();
   if (off) return false;
+  static const int max_l_env = [] {  // BD_SMALL_MAXL: development A/B of the L range
+    const char* e = getenv("BD_SMALL_MAXL");
+    return e != nullptr ? atoi(e) : 4 * tc::BM;  // row blocks of pairs up to L = 512
+  }();
+  static const bool wide = [] {  // BD_SMALL_WIDE=1: pairs also for wide problems
+    const char* e = getenv("BD_SMALL_WIDE");
+    return e != nullptr && atoi(e) == 1;
+  }();
   int64_t cols = 0, max_l = 0;
   for (int i = 0; i < count; ++i) {
-    if (probs[i].L > 2 * tc::BM || probs[i].K > tc::SM_MAX_KB * tc::BK || probs[i].world > 0 ||
+    if (probs[i].L > max_l_env || probs[i].K > tc::SM_MAX_KB * tc::BK || probs[i].world > 0 ||
         probs[i].rep_gamma != nullptr)
       return false;
     cols += probs[i].N;
     max_l = probs[i].L > max_l ? probs[i].L : max_l;
   }
-  // 128 < L <= 256 (CTA pairs): only while 128-column blocks fill at most one wave of
-  // pairs — with 256-column blocks its 4-warp direct-store epilogue loses to the
-  // persistent kernel (measured: n = 128 heads, L = 256: 10.5 vs 8.1 us)
-  if (max_l > tc::BM && cols > static_cast<int64_t>(sm_count() / 2) * 128) return false;
+  // L > 128 (CTA pairs): only while 128-column blocks fill at most one wave of pairs
+  // per row block — wider problems run faster on the persistent kernel (measured: n =
+  // 128 heads, L = 256: 10.5 vs 8.1 us)
+  const int64_t nrb = (max_l + 2 * tc::BM - 1) / (2 * tc::BM);
+  if (!wide && max_l > tc::BM && nrb * cols > static_cast<int64_t>(sm_count() / 2) * 128)
+    return false;
   return true;
 }
+
+#ifdef BD_WITH_DECODE_EXPERIMENT
+// tools/experiments/kv_proj_decode.cu (development builds only, see its header)
+bool decode_eligible(const Problem* probs, int count);
+int launch_decode(const Problem* probs, int count, bool bf16, int* flag, cudaStream_t stream);
+#endif
 
 int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_t stream) {
   using namespace tc;
   const bool bf16 = dtype == BD_BF16;
+#ifdef BD_WITH_DECODE_EXPERIMENT
+  if (decode_eligible(probs, count)) return launch_decode(probs, count, bf16, flag, stream);
+#endif
   if (small_eligible(probs, count)) return launch_small(probs, count, bf16, flag, stream);
   TcParams prm;
   {
