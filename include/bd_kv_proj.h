@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define BD_KV_PROJ_ABI_VERSION 5
+#define BD_KV_PROJ_ABI_VERSION 6
 
 /* element types */
 enum bd_dtype { BD_F32 = 0, BD_F64 = 1, BD_F16 = 2, BD_BF16 = 3 };
@@ -178,6 +178,29 @@ int bd_kv_proj_grouped_allgather(const bd_kv_problem* problems, int count, int d
 int bd_kv_proj_grouped_rmsnorm(const bd_kv_problem* problems, int count, int dtype, int mode,
                                int out_layout, const float* const* rep_gamma, float eps,
                                int* nonfinite_flag, void* stream);
+
+/*
+ * Causal (or full) prefill attention of the BD-rewritten DeepSeek-V2 MLA block, reading the
+ * BD projection's outputs in place (BD ⊕ FlashAttention; the attention
+ * core the reference computes after its two fused_kv_proj calls, ref
+ * pkg/src/bdattn/attention.py:298-307 and _attend :143-154, restated for MLA):
+ *   out[t, h, :] = softmax_s(scale * (q[t, h, 0:dn] . k_nope[h, s, :] + q[t, h, dn:] . k_pe[s, :]))
+ *                  @ v[h, s, :]
+ * q:      element (t, h, c) at q + t*ldq_tok + h*ldq_head + c, c < d_nope + d_rope
+ * k_nope: (h, s, c) at k_nope + h*k_head_stride + s*ldk + c   (head-major, BD out_layout=head)
+ * k_pe:   (s, c) at k_pe + s*ldkpe + c — the decoupled RoPE key, shared by every head
+ * v:      (h, s, c) at v + h*v_head_stride + s*ldv + c        (head-major)
+ * out:    (t, h, c) at out + t*ldo_tok + h*ldo_head + c
+ * causal: key s attends to query t only for s <= t.  dtype F16/BF16; geometry d_nope = 128,
+ * d_rope = 64, d_v = 128 (DeepSeek-V2 / -V2-Lite); 16-byte aligned pointers, strides
+ * multiples of 8 elements.  Returns BD_OK or BD_ERR_*; asynchronous on `stream`.
+ */
+int bd_mla_attention(const void* q, int64_t ldq_tok, int64_t ldq_head, const void* k_nope,
+                     int64_t ldk, int64_t k_head_stride, const void* k_pe, int64_t ldkpe,
+                     const void* v, int64_t ldv, int64_t v_head_stride, void* out,
+                     int64_t ldo_tok, int64_t ldo_head, int64_t L, int64_t n_heads,
+                     int64_t d_nope, int64_t d_rope, int64_t d_v, float scale, int causal,
+                     int dtype, void* stream);
 
 /* Human-readable description of the last error on this thread ("" if none). */
 const char* bd_last_error(void);

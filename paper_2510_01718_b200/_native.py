@@ -22,7 +22,7 @@ BD_F32, BD_F64, BD_F16, BD_BF16 = 0, 1, 2, 3
 BD_OK, BD_ERR_SHAPE, BD_ERR_DTYPE, BD_ERR_ALIGN, BD_ERR_CUDA, BD_ERR_ARG = 0, 1, 2, 3, 4, 5
 BD_MODE_AUTO, BD_MODE_EXACT, BD_MODE_TC = 0, 1, 2
 BD_MAX_GROUP = 4
-ABI_VERSION = 5
+ABI_VERSION = 6
 BD_MAX_PEERS = 8
 BD_OUT_TOKEN_MAJOR, BD_OUT_HEAD_MAJOR = 0, 1
 BD_TAG_FIRST, BD_TAG_LAST = 0, 1
@@ -36,6 +36,7 @@ EXPORTED_SYMBOLS = (
     "bd_kv_proj_host",
     "bd_matmul",
     "bd_linear_forward",
+    "bd_mla_attention",
     "bd_last_error",
     "bd_abi_version",
     "bd_launch_count",
@@ -99,6 +100,9 @@ def load() -> ctypes.CDLL:
     lib.bd_linear_forward.argtypes = [vp, i64, vp, i64, vp, i64, vp, i64, i64, i64, i64, i64, ci,
                                       ci, ci, vp, vp]
     lib.bd_linear_forward.restype = ci
+    lib.bd_mla_attention.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64, vp, i64, i64, vp, i64,
+                                     i64, i64, i64, i64, i64, i64, ctypes.c_float, ci, ci, vp]
+    lib.bd_mla_attention.restype = ci
     lib.bd_last_error.argtypes = []
     lib.bd_last_error.restype = ctypes.c_char_p
     lib.bd_abi_version.argtypes = []

@@ -18,7 +18,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libbd_kvproj.so"
-SOURCES = ["capi.cu", "kv_proj_exact.cu", "kv_proj_tc.cu"]
+SOURCES = ["capi.cu", "kv_proj_exact.cu", "kv_proj_tc.cu", "mla_attn.cu"]
 HEADERS = ["ptx_sm100.cuh", "kv_proj_internal.h", "tc_common.cuh"]
 
 NVCC_FLAGS = [

@@ -414,6 +414,35 @@ int bd_linear_forward(const void* x, int64_t ldx, const void* basis, int64_t ldb
   return dispatch(&p2, 1, dtype, m, nonfinite_flag, s);
 }
 
+int bd_mla_attention(const void* q, int64_t ldq_tok, int64_t ldq_head, const void* k_nope,
+                     int64_t ldk, int64_t k_head_stride, const void* k_pe, int64_t ldkpe,
+                     const void* v, int64_t ldv, int64_t v_head_stride, void* out,
+                     int64_t ldo_tok, int64_t ldo_head, int64_t L, int64_t n_heads,
+                     int64_t d_nope, int64_t d_rope, int64_t d_v, float scale, int causal,
+                     int dtype, void* stream) {
+  using namespace bdk;
+  g_last_error.clear();
+  if (q == nullptr || k_nope == nullptr || k_pe == nullptr || v == nullptr || out == nullptr)
+    return fail(BD_ERR_ARG, "bd_mla_attention: null pointer");
+  if (dtype != BD_F16 && dtype != BD_BF16)
+    return fail(BD_ERR_DTYPE, "bd_mla_attention: F16/BF16 only");
+  if (L < 1 || n_heads < 1 || L > INT32_MAX / 2 || n_heads > 65535)
+    return fail(BD_ERR_SHAPE, "bd_mla_attention: invalid L or n_heads");
+  if (d_nope != 128 || d_rope != 64 || d_v != 128)
+    return fail(BD_ERR_SHAPE, "bd_mla_attention: supported geometry is d_nope=128, d_rope=64, d_v=128");
+  if (!(scale > 0.f)) return fail(BD_ERR_ARG, "bd_mla_attention: scale must be > 0");
+  if (ldq_head < d_nope + d_rope || ldq_tok < ldq_head * n_heads || ldk < d_nope ||
+      k_head_stride < ldk * L || ldkpe < d_rope || ldv < d_v || v_head_stride < ldv * L ||
+      ldo_head < d_v || ldo_tok < ldo_head * n_heads)
+    return fail(BD_ERR_SHAPE, "bd_mla_attention: strides too small for the layouts");
+  if (!aligned16(q) || !aligned16(k_nope) || !aligned16(k_pe) || !aligned16(v) || !aligned16(out) ||
+      ((ldq_tok | ldq_head | ldk | k_head_stride | ldkpe | ldv | v_head_stride | ldo_tok | ldo_head) & 7))
+    return fail(BD_ERR_ALIGN, "bd_mla_attention: 16-byte aligned pointers and strides needed");
+  MlaAttnArgs a{q, ldq_tok, ldq_head, k_nope, ldk, k_head_stride, k_pe, ldkpe, v, ldv,
+                v_head_stride, out, ldo_tok, ldo_head, L, n_heads, scale, causal, dtype};
+  return launch_mla_attention(a, static_cast<cudaStream_t>(stream));
+}
+
 const char* bd_last_error(void) { return bdk::g_last_error.c_str(); }
 
 int bd_abi_version(void) { return BD_KV_PROJ_ABI_VERSION; }

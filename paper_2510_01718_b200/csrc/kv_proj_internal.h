@@ -49,6 +49,26 @@ cudaError_t launch_exact(const Problem* probs, int count, int dtype, int* flag,
 // tcgen05 tensor-core kernel (FP16/BF16). Returns BD_* status; sets error text.
 int launch_tc(const Problem* probs, int count, int dtype, int* flag, cudaStream_t stream);
 
+// MLA prefill attention over the BD projection's outputs (mla_attn.cu): Q [L][H][192]
+// token-major, K'_nope / V' head-major [H][L][128], the shared RoPE key k_pe [L][64].
+struct MlaAttnArgs {
+  const void* q;
+  int64_t ldq_tok, ldq_head;
+  const void* k_nope;
+  int64_t ldk, k_head_stride;
+  const void* k_pe;
+  int64_t ldkpe;
+  const void* v;
+  int64_t ldv, v_head_stride;
+  void* out;
+  int64_t ldo_tok, ldo_head;
+  int64_t L, n_heads;
+  float scale;
+  int causal;
+  int dtype;
+};
+int launch_mla_attention(const MlaAttnArgs& a, cudaStream_t stream);
+
 // SM count of the current device (cached).
 int sm_count();
 

@@ -40,8 +40,10 @@ from torch.nn.attention import SDPBackend, sdpa_kernel
 
 from .attention import select_tag
 from .decompose import Axis, Tag, bd_decompose_both, ordered_matmul
-from .errors import ShapeError
-from .kv_proj import fold_rmsnorm, fused_kv_proj_grouped, fused_rmsnorm_kv_proj_grouped
+from . import _native as _N
+from .errors import NativeLibraryError, PrecisionError, ShapeError
+from .kv_proj import (_on_device, fold_rmsnorm, fused_kv_proj_grouped,
+                      fused_rmsnorm_kv_proj_grouped)
 
 
 # attention-core backends, in preference order (cuDNN first: it supports the MLA head
@@ -272,16 +274,74 @@ def mla_forward(hidden: torch.Tensor, w: MLAWeights, *, causal: bool = True) -> 
     return o @ w.w_o
 
 
+def mla_attention(q: torch.Tensor, k_nope: torch.Tensor, k_pe: torch.Tensor, v: torch.Tensor,
+                  *, scale: float, causal: bool = True,
+                  out: torch.Tensor | None = None) -> torch.Tensor:
+    """MLA prefill attention on the tcgen05 kernel (``bd_mla_attention``, csrc/mla_attn.cu):
+
+        out[t, h] = softmax_s(scale (q[t,h,:128] . k_nope[h,s] + q[t,h,128:] . k_pe[s])) v[h,s]
+
+    ``q`` [L, H, 192] (last dim contiguous; any token / head strides), ``k_nope`` and ``v``
+    head-major [H, L, 128] — the BD projection's ``out_layout="head"`` outputs, read in
+    place — and ``k_pe`` [L, 64], the RoPE key shared by all heads (never broadcast).
+    Returns [L, H, 128] (or writes ``out``).  FP16/BF16 CUDA tensors; no fallback.
+    """
+    if q.dim() != 3 or k_nope.dim() != 3 or v.dim() != 3 or k_pe.dim() != 2:
+        raise ShapeError("q [L,H,192], k_nope [H,L,128], k_pe [L,64], v [H,L,128] expected")
+    L, H, dq = q.shape
+    if tuple(k_nope.shape) != (H, L, 128) or tuple(v.shape) != (H, L, 128) or \
+            tuple(k_pe.shape) != (L, 64) or dq != 192:
+        raise ShapeError(f"inconsistent shapes q{tuple(q.shape)} k_nope{tuple(k_nope.shape)} "
+                         f"k_pe{tuple(k_pe.shape)} v{tuple(v.shape)}")
+    dt = q.dtype
+    if any(t.dtype != dt for t in (k_nope, k_pe, v)) or dt not in (torch.float16, torch.bfloat16):
+        raise PrecisionError("mla_attention: q, k_nope, k_pe, v must share float16/bfloat16")
+    if not all(t.is_cuda for t in (q, k_nope, k_pe, v)):
+        raise NativeLibraryError("mla_attention needs CUDA tensors (no CPU fallback)")
+    if any(t.stride(-1) != 1 for t in (q, k_nope, k_pe, v)):
+        raise ShapeError("mla_attention: the last dimension must be contiguous")
+    if out is None:
+        out = torch.empty((L, H, 128), dtype=dt, device=q.device)
+    elif tuple(out.shape) != (L, H, 128) or out.dtype != dt or out.stride(-1) != 1:
+        raise ShapeError("out must be [L, H, 128] of q's dtype with a contiguous last dim")
+    st = _on_device(q.device, _N.load().bd_mla_attention,
+                    q.data_ptr(), q.stride(0), q.stride(1),
+                    k_nope.data_ptr(), k_nope.stride(1), k_nope.stride(0),
+                    k_pe.data_ptr(), k_pe.stride(0),
+                    v.data_ptr(), v.stride(1), v.stride(0),
+                    out.data_ptr(), out.stride(0), out.stride(1),
+                    L, H, 128, 64, 128, float(scale), 1 if causal else 0,
+                    _N.BD_F16 if dt == torch.float16 else _N.BD_BF16)
+    _N.check(st, "bd_mla_attention")
+    return out
+
+
 def bd_mla_forward(hidden: torch.Tensor, w: BDMLAWeights, *, causal: bool = True,
-                   group=None, fuse_norm: bool = True) -> torch.Tensor:
+                   group=None, fuse_norm: bool = True, attention: str = "sdpa",
+                   head_group: int | None = None) -> torch.Tensor:
     """BD MLA block: K'_nope and V' of all (local) heads in ONE launch of the BD kernel,
     with kv_a_layernorm fused into it (``fuse_norm``, when the weights carry the fold:
     the raw latent is read once and never normalised in memory).  With head-sharded
     weights (``shard_bd_mla``) the partial outputs are summed with one all_reduce over
-    ``group``."""
+    ``group``.
+
+    ``attention="sdpa"``: the attention core is torch SDPA (cuDNN) on [K'_nope | k_pe]
+    per head.  ``attention="bd"`` (16-bit, DeepSeek-V2 head geometry): the tcgen05 kernel
+    ``mla_attention`` reads K'_nope / V' head-major and the shared k_pe in place — no
+    key concatenation, no RoPE-key broadcast — and, with ``head_group = G``, the block
+    runs G heads at a time: the BD projection of a group's K'/V' into a 2-deep ring of
+    group buffers sized to stay in L2, then the attention over them, so K'/V' go from the
+    projection's epilogue to the attention's TMA loads through L2 instead of a round
+    trip through HBM (SURVEY §8(f) #3)."""
     cfg, H = w.cfg, w.n_heads
     L = hidden.shape[0]
-    q_nope, q_pe = _split_q(hidden @ w.w_q, H, cfg)
+    if attention not in ("sdpa", "bd"):
+        raise ValueError(f"attention must be 'sdpa' or 'bd', not {attention!r}")
+    use_bd_attn = attention == "bd"
+    if use_bd_attn and (hidden.dtype not in (torch.float16, torch.bfloat16) or cfg.qk_nope != 128
+                        or cfg.qk_rope != 64 or cfg.v_head != 128):
+        raise ShapeError("attention='bd' needs 16-bit activations and nope/rope/v = 128/64/128")
+    q = hidden @ w.w_q
     # fused norm: exact kernel (float32/64) any shape; tensor cores need the latent row
     # resident (d_h in {64, 128}, kv_lora - d_h <= 384 — DeepSeek-V2-Lite's 128 / 384)
     fused = fuse_norm and w.norm_fold is not None and (
@@ -294,29 +354,55 @@ def bd_mla_forward(hidden: torch.Tensor, w: BDMLAWeights, *, causal: bool = True
     else:
         c_kv, k_pe = _latent(hidden, w.w_kva, w.kva_norm, cfg)
     rope = lambda t: _rope(t, cfg.rope_theta, cfg.rope_interleaved)  # noqa: E731
-    # The BD kernel writes K'_nope head-major straight into the first qk_nope columns of
-    # the attention key buffer [H, L, nope + rope] (row stride nope + rope) and V'
-    # head-major into [H, L, v]: the SDPA operands need no transpose or concatenation
-    # copy of K'/V'; only the shared RoPE key part is broadcast into each head's tail.
-    k_buf = torch.empty((H, L, cfg.qk_head), dtype=c_kv.dtype, device=c_kv.device)
-    v_buf = torch.empty((H, L, cfg.v_head), dtype=c_kv.dtype, device=c_kv.device)
-    outs = [k_buf[..., :cfg.qk_nope], v_buf]
-    if fused:
-        cq, cv, gq, gv = w.norm_fold
-        fused_rmsnorm_kv_proj_grouped(c_kv, [(cq, gq, cfg.qk_nope, H, w.qk_tag),
-                                             (cv, gv, cfg.v_head, H, w.vo_tag)], cfg.rms_eps,
-                                      outs=outs, out_layout="head", check_finite=False)
+
+    def project(h0, h1, k_out, v_out):
+        dn, dv = cfg.qk_nope, cfg.v_head
+        if fused:
+            cq, cv, gq, gv = w.norm_fold
+            fused_rmsnorm_kv_proj_grouped(
+                c_kv, [(cq[:, h0 * dn:h1 * dn], gq, dn, h1 - h0, w.qk_tag),
+                       (cv[:, h0 * dv:h1 * dv], gv, dv, h1 - h0, w.vo_tag)], cfg.rms_eps,
+                outs=[k_out, v_out], out_layout="head", check_finite=False)
+        else:
+            fused_kv_proj_grouped(
+                c_kv, [(w.c_qk[:, h0 * dn:h1 * dn], dn, h1 - h0, w.qk_tag),
+                       (w.c_vo[:, h0 * dv:h1 * dv], dv, h1 - h0, w.vo_tag)],
+                outs=[k_out, v_out], out_layout="head", check_finite=False)
+
+    if use_bd_attn:
+        qv = q.view(L, H, cfg.qk_head)
+        qv[..., cfg.qk_nope:] = rope(qv[..., cfg.qk_nope:])   # RoPE in place, no concat
+        k_pe_r = rope(k_pe).contiguous()
+        scale = 1.0 / math.sqrt(cfg.qk_head)
+        o = torch.empty((L, H, cfg.v_head), dtype=q.dtype, device=q.device)
+        G = H if head_group is None else max(1, min(H, int(head_group)))
+        ring = [(torch.empty((G, L, cfg.qk_nope), dtype=q.dtype, device=q.device),
+                 torch.empty((G, L, cfg.v_head), dtype=q.dtype, device=q.device))
+                for _ in range(1 if G == H else 2)]
+        for gi, h0 in enumerate(range(0, H, G)):
+            h1 = min(H, h0 + G)
+            kb, vb = ring[gi % len(ring)]
+            kb, vb = kb[:h1 - h0], vb[:h1 - h0]
+            project(h0, h1, kb, vb)
+            mla_attention(qv[:, h0:h1], kb, k_pe_r, vb, scale=scale, causal=causal,
+                          out=o[:, h0:h1])
+        out = o.view(L, H * cfg.v_head) @ w.b_vo
     else:
-        fused_kv_proj_grouped(c_kv, [(w.c_qk, cfg.qk_nope, H, w.qk_tag),
-                                     (w.c_vo, cfg.v_head, H, w.vo_tag)],
-                              outs=outs, out_layout="head", check_finite=False)
-    k_buf[..., cfg.qk_nope:] = rope(k_pe)[None]
-    q = torch.cat([q_nope.view(L, H, cfg.qk_nope), rope(q_pe).view(L, H, cfg.qk_rope)], -1)
-    with sdpa_kernel(_BACKENDS):
-        o = F.scaled_dot_product_attention(q.transpose(0, 1)[None], k_buf[None], v_buf[None],
-                                           is_causal=causal, scale=1.0 / math.sqrt(cfg.qk_head))
-    o = o[0].transpose(0, 1).reshape(L, H * cfg.v_head)
-    out = o @ w.b_vo
+        # The BD kernel writes K'_nope head-major straight into the first qk_nope columns
+        # of the attention key buffer [H, L, nope + rope] (row stride nope + rope) and V'
+        # head-major into [H, L, v]: the SDPA operands need no transpose or concatenation
+        # copy of K'/V'; only the shared RoPE key part is broadcast into each head's tail.
+        k_buf = torch.empty((H, L, cfg.qk_head), dtype=c_kv.dtype, device=c_kv.device)
+        v_buf = torch.empty((H, L, cfg.v_head), dtype=c_kv.dtype, device=c_kv.device)
+        project(0, H, k_buf[..., :cfg.qk_nope], v_buf)
+        k_buf[..., cfg.qk_nope:] = rope(k_pe)[None]
+        q_nope, q_pe = _split_q(q, H, cfg)
+        q = torch.cat([q_nope.view(L, H, cfg.qk_nope), rope(q_pe).view(L, H, cfg.qk_rope)], -1)
+        with sdpa_kernel(_BACKENDS):
+            o = F.scaled_dot_product_attention(q.transpose(0, 1)[None], k_buf[None], v_buf[None],
+                                               is_causal=causal, scale=1.0 / math.sqrt(cfg.qk_head))
+        o = o[0].transpose(0, 1).reshape(L, H * cfg.v_head)
+        out = o @ w.b_vo
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(out, group=group)
     return out
