@@ -21,7 +21,7 @@ def rep(a, b):
 
 
 i = s.index("namespace bdk {")
-s = (s[:i] + "__device__ unsigned long long g_tl[148][64];\n"
+s = (s[:i] + "__device__ unsigned long long g_tl[148][96];\n"
      + '#define GT() ({unsigned long long _g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_g)); _g;})\n'
      + "#define CK() ((unsigned long long)clock64())\n" + s[i:])
 s += '''
@@ -54,7 +54,7 @@ rep('''  tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;''')
 rep('''      griddep_wait();
       for (int t = t_begin; t < t_end; t += t_step) {''', '''      griddep_wait();
-      if (lane == 0) TL[6] = CK();
+      if (lane == 0) { TL[6] = CK(); TL[45] = GT(); }
       for (int t = t_begin; t < t_end; t += t_step) {''')
 for lead in ("0", "lead"):
     a = f'''            const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), {lead});'''
