@@ -531,16 +531,53 @@ def run_block(args, torch, dist, dev, rank, world, dtype, stream):
 
     bd_ms = time_fn(lambda: M.bd_mla_forward(hid, p))
     dense_ms = time_fn(lambda: M.mla_forward(hid, wd)) if world == 1 else None
+    # the tcgen05 MLA attention kernel reading K'/V' head-major in place:
+    # whole block, and in head groups of 4 through the L2 ring of group buffers
+    bd_attn_ms = time_fn(lambda: M.bd_mla_forward(hid, p, attention="bd"))
+    bd_attn_g4_ms = time_fn(lambda: M.bd_mla_forward(hid, p, attention="bd", head_group=4))
     out = {"workload": "cfg5: DeepSeek-V2-Lite MLA block (hidden 2048, 16 heads, kv_lora 512, "
                        "nope/rope/v 128/64/128), causal, random-init, BD kv_b_proj",
            "tokens": L, "heads_per_gpu": cfg.n_heads // world, "scaling": "strong",
            "bd_ms": bd_ms, "bd_tokens_per_s": L / (bd_ms * 1e-3),
            "bd_flops_per_gpu": M.block_flops(L, cfg, cfg.n_heads // world, bd=True),
-           "qk_tag": p.qk_tag.value, "vo_tag": p.vo_tag.value}
+           "qk_tag": p.qk_tag.value, "vo_tag": p.vo_tag.value,
+           "bd_attention": {"ms": bd_attn_ms, "head_group_4_ms": bd_attn_g4_ms,
+                            "what": "BD block with attention='bd' (csrc/mla_attn.cu) instead of "
+                                    "cuDNN SDPA; head_group_4: K'/V' of 4 heads at a time "
+                                    "through an L2-sized ring"}}
     if dense_ms is not None:
         out.update({"dense_ms": dense_ms, "dense_tokens_per_s": L / (dense_ms * 1e-3),
                     "speedup_vs_dense": dense_ms / bd_ms})
+        out["breakdown"] = block_breakdown(torch, M, hid, w, wd, p, time_fn, dense_ms, bd_ms)
     return out
+
+
+def block_breakdown(torch, M, hid, w, wd, p, time_fn, dense_ms, bd_ms):
+    """Where the BD block's gain over the dense block comes from:
+    the kv_b projection itself (BD kernel head-major vs cuBLAS, same tokens), the fused
+    kv_a_layernorm (the BD block with fuse_norm=False), and the rest — the head-major
+    K'/V' written straight into the SDPA operands instead of the dense block's
+    view/reshape/cat copies."""
+    from paper_2510_01718_b200.kv_proj import fused_kv_proj_grouped
+    cfg = w.cfg
+    L, H = hid.shape[0], cfg.n_heads
+    unfused_ms = time_fn(lambda: M.bd_mla_forward(hid, p, fuse_norm=False))
+    c_kv = torch.randn(L, cfg.kv_lora_rank, device=hid.device, dtype=hid.dtype)
+    kvb = torch.empty(L, wd.w_kvb.shape[1], device=hid.device, dtype=hid.dtype)
+    dense_proj_ms = time_fn(lambda: torch.matmul(c_kv, wd.w_kvb, out=kvb))
+    kb = torch.empty(H, L, cfg.qk_nope, device=hid.device, dtype=hid.dtype)
+    vb = torch.empty(H, L, cfg.v_head, device=hid.device, dtype=hid.dtype)
+    specs = [(p.c_qk, cfg.qk_nope, H, p.qk_tag), (p.c_vo, cfg.v_head, H, p.vo_tag)]
+    bd_proj_ms = time_fn(lambda: fused_kv_proj_grouped(c_kv, specs, outs=[kb, vb], out_layout="head",
+                                                      check_finite=False))
+    proj = dense_proj_ms - bd_proj_ms
+    norm = unfused_ms - bd_ms
+    return {"dense_ms": dense_ms, "bd_ms": bd_ms, "bd_unfused_norm_ms": unfused_ms,
+            "kv_b_proj_dense_ms": dense_proj_ms, "kv_b_proj_bd_ms": bd_proj_ms,
+            "gain_ms": {"kv_b_projection": proj, "fused_rmsnorm": norm,
+                        "layout_and_rest": dense_ms - bd_ms - proj - norm},
+            "note": "gain = dense_ms - bd_ms split by source; the BD FLOP saving is 0.54% of "
+                    "the block (SURVEY 8(d)), the projection term is what BD itself buys"}
 
 
 # ----------------------------------------------------------------------------- configs
