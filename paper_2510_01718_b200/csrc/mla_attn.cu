@@ -338,6 +338,11 @@ __global__ void __launch_bounds__(THREADS, 1) mla_attn_kernel(const __grid_const
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[sb]);
         ++pv_it;  // PV_j will be the pv_it-th PV issued
+        // Observe every pv_done phase (PV_{j-1}: long complete by now, so this costs a
+        // single probe).  The lazy rescale above waits only when the max moved; without
+        // this wait most phases would complete unobserved (correct — a waiter can never
+        // fall two phases behind — but flagged by compute-sanitizer's synccheck).
+        if (j > 0) mbar_wait(pv_done, (pv_it - 2) & 1u);
       }
       // epilogue: O / l, straight to global (this thread's row is 256 contiguous bytes)
       mbar_wait(pv_done, (pv_it - 1) & 1u);

@@ -83,6 +83,30 @@ def main():
     y = bd.bd_linear_forward(torch.randn(300, 256, generator=g).half().to(dev),
                              bd.BDLinearLayer(fac, basis, coeff))
     assert bool(torch.isfinite(y).all())
+    # tcgen05 MLA prefill attention (csrc/mla_attn.cu): causal with a ragged last tile,
+    # non-causal, a strided q view; FP16 and BF16, vs float64
+    from paper_2510_01718_b200 import mla as M
+    for dt in (torch.float16, torch.bfloat16):
+        for L, H, causal in ((300, 2, True), (200, 3, False)):
+            q = torch.randn(L, H, 192, generator=g).to(dt).to(dev)
+            kn = torch.randn(H, L, 128, generator=g).to(dt).to(dev)
+            kpe = torch.randn(L, 64, generator=g).to(dt).to(dev)
+            vv = torch.randn(H, L, 128, generator=g).to(dt).to(dev)
+            sc = 1.0 / 192 ** 0.5
+            o = M.mla_attention(q, kn, kpe, vv, scale=sc, causal=causal)
+            qd, kd, pd, vd = (t.double() for t in (q, kn, kpe, vv))
+            for h in range(H):
+                sm = (qd[:, h, :128] @ kd[h].T + qd[:, h, 128:] @ pd.T) * sc
+                if causal:
+                    sm.masked_fill_(torch.ones(L, L, dtype=torch.bool, device=dev).triu(1),
+                                    float("-inf"))
+                err = float((o[:, h].double() - torch.softmax(sm, -1) @ vd[h]).abs().max())
+                assert err < (2e-2 if dt == torch.bfloat16 else 3e-3), (dt, L, H, h, err)
+        wide = torch.randn(256, 4, 256, generator=g).to(dt).to(dev)[..., :192]
+        o = M.mla_attention(wide, torch.randn(4, 256, 128, generator=g).to(dt).to(dev),
+                            torch.randn(256, 64, generator=g).to(dt).to(dev),
+                            torch.randn(4, 256, 128, generator=g).to(dt).to(dev), scale=0.07)
+        assert bool(torch.isfinite(o).all())
     torch.cuda.synchronize()
     print("sanitize_run: all variants ok")
 
