@@ -1217,7 +1217,7 @@ bool small_eligible(const Problem* probs, int count) {
 }
 
 #ifdef BD_WITH_DECODE_EXPERIMENT
-// tools/experiments/kv_proj_decode.cu (development builds only, see its header)
+// tools/experiments/kv_proj_decode_splitk.cu (development builds only, see its header)
 bool decode_eligible(const Problem* probs, int count);
 int launch_decode(const Problem* probs, int count, bool bf16, int* flag, cudaStream_t stream);
 #endif

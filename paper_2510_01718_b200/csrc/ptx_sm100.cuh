@@ -94,6 +94,12 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
                ::: "memory");
 }
+// Cluster barrier whose arrive does not order this thread's prior memory operations (no
+// release fence waiting on outstanding loads or prefetches); mbarrier initialisation is
+// published to the cluster by fence.mbarrier_init.release.cluster before it.
+__device__ __forceinline__ void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
 // Arrive (default .release.cta semantics) on an mbarrier given by its shared::cluster
 // address, e.g. the pair leader's.  Cluster-scope release is avoided on purpose: it
 // compiles to a fence that waits for this thread's outstanding memory operations.

@@ -49,13 +49,16 @@ struct TcParams {
   int32_t head0[BD_MAX_GROUP];
   int32_t count;
   int32_t total_tiles;  // tiles of (BM * CG) rows x BN columns
-  int32_t a_kb_bytes;   // small-L kernel: bytes of one A k-block (rows rounded to 8 x 128 B)
+  int32_t a_kb_bytes;   // small-L / decode kernels: bytes of one A k-block (rows rounded
+                        // to 8 x 128 B)
   int32_t strided;      // tiles dealt round-robin to the pairs (streaming-A problems)
   int32_t norm;         // fused RMSNorm (kNorm variant)
   int* flag;            // non-finite flag (kCheck instantiation only)
-  int32_t dbg_seq;      // launch sequence number (decode kernel's stamp builds only)
-  int32_t dc_stages;    // decode kernel experiment: ring stages and ring bytes
-  int32_t dc_ring_bytes;
+  int32_t dk_kps;         // decode kernel: k-blocks of 64 per CTA (problem p splits its
+                          // contraction over ceil(num_kb / dk_kps) CTAs of a cluster)
+  int32_t dk_a_bytes;     // decode kernel: A region, B region and receive buffer bytes
+  int32_t dk_b_bytes;
+  int32_t dk_recv_bytes;
   int32_t small_rblocks;  // small-L kernel: row blocks of BM * CGS rows (grid = cols x rows)
 };
 

@@ -1,6 +1,6 @@
-// kv_proj_decode.cu — EXPERIMENT (not in the product library): a decode-sized-L (<= 256)
-// BD K/V projection kernel.  Built only by tools/build_variant.sh with WITH_DECODE=1
-// (BD_WITH_DECODE_EXPERIMENT); measured against the shipped small-L kernel in round 2 and
+// kv_proj_decode_ring.cu — EXPERIMENT (not in the product library; no longer builds:
+// its TcParams fields were reused by kv_proj_decode_splitk.cu): a decode-sized-L (<= 256)
+// BD K/V projection kernel, measured against the shipped small-L kernel in round 2 and
 // NOT better overall (wins at L = 1 / cfg2 L = 64, loses at L = 64-256
 // on the paper shape).  Kept for the record of what was tried.
 //
