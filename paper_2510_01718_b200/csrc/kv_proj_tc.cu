@@ -66,9 +66,9 @@ namespace tc {
 
 constexpr int CG = 2;                         // cta_group::2 (CTA pairs)
 constexpr int BM = 128;                       // rows per CTA per tile (TMEM lanes)
-constexpr int BN = 256;                       // UMMA N (output columns per pair tile)
+constexpr int BN = 256;                       // UMMA N (output columns per pair tile); short
+                                              // launches use 128-wide tiles (template BNT)
 constexpr int NUM_ACC = 512 / BN;             // accumulator buffers in TMEM's 512 columns
-static_assert(BN == 256, "the epilogue's column mapping assumes 256-wide tiles");
 constexpr int BK = 64;                        // A k-block: one 128-byte swizzle row of A
 constexpr int BKB = 64;                       // B k-block (BKB = 32 with 8 stages: +4 us)
 constexpr int B_SUB = BK / BKB;               // B stages per A k-block
@@ -89,15 +89,17 @@ constexpr uint32_t TMEM_COLS = 512;          // NUM_ACC accumulator buffers
 constexpr uint32_t NORM_SCRATCH = 2 * BM * 4;  // kNorm: per-row partial sums of squares
 constexpr size_t SMEM_BYTES = 1024 + A_SLOTS * A_BYTES + B_STAGES * B_BYTES + REP_BYTES +
                               EPI_WARPS * STG_BUFS * STG_BYTES + 512 + NORM_SCRATCH;
-static_assert((2 * A_SLOTS + 2 * B_STAGES + 2 * NUM_ACC + 1) * 8 + 4 <= 512, "barrier area");
+// 128-wide tiles: twice the B stages (same ring bytes) and four accumulator buffers
+static_assert((2 * A_SLOTS + 2 * 2 * B_STAGES + 2 * 2 * NUM_ACC + 1) * 8 + 4 <= 512, "barrier area");
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
+template <int BNT = BN>
 __device__ __forceinline__ void decode_tile(const TcParams& prm, int t, int& pi, int& m0,
                                             int& n0) {
   pi = 0;
   while (pi + 1 < prm.count && t >= prm.p[pi + 1].tile_start) ++pi;
   const int local = t - prm.p[pi].tile_start;
-  n0 = (local % prm.p[pi].tiles_n) * BN;
+  n0 = (local % prm.p[pi].tiles_n) * BNT;
   m0 = (local / prm.p[pi].tiles_n) * (BM * CG);
 }
 
@@ -107,35 +109,37 @@ __device__ __forceinline__ void decode_tile(const TcParams& prm, int t, int& pi,
 // division + indexed parameter loads) cost ~700 clocks per tile.
 struct TileCursor {
   int pi, m0, n0;
-  int n_span;    // tiles_n * BN of problem pi
+  int n_span;    // tiles_n * BNT of problem pi
   int pend;      // first tile of problem pi + 1
   int t;
   int step;      // tile stride between this pair's consecutive tiles (1: contiguous)
 };
+template <int BNT>
 __device__ __forceinline__ void cursor_load(const TcParams& prm, TileCursor& c) {
-  c.n_span = prm.p[c.pi].tiles_n * BN;
+  c.n_span = prm.p[c.pi].tiles_n * BNT;
   c.pend = c.pi + 1 < prm.count ? prm.p[c.pi + 1].tile_start : 0x7fffffff;
 }
+template <int BNT>
 __device__ __forceinline__ TileCursor cursor_at(const TcParams& prm, int t, int step) {
   TileCursor c;
   c.t = t;
   c.step = step;
-  decode_tile(prm, t, c.pi, c.m0, c.n0);
-  cursor_load(prm, c);
+  decode_tile<BNT>(prm, t, c.pi, c.m0, c.n0);
+  cursor_load<BNT>(prm, c);
   return c;
 }
-template <bool kRR>
+template <bool kRR, int BNT>
 __device__ __forceinline__ void cursor_next(const TcParams& prm, TileCursor& c) {
   if constexpr (kRR) {  // round-robin tiles (long K): a full decode is off the critical path
     c.t += c.step;
     if (c.t < prm.total_tiles) {
-      decode_tile(prm, c.t, c.pi, c.m0, c.n0);
-      cursor_load(prm, c);
+      decode_tile<BNT>(prm, c.t, c.pi, c.m0, c.n0);
+      cursor_load<BNT>(prm, c);
     }
     return;
   }
   ++c.t;
-  c.n0 += BN;
+  c.n0 += BNT;
   if (c.n0 >= c.n_span) {
     c.n0 = 0;
     c.m0 += BM * CG;
@@ -144,7 +148,7 @@ __device__ __forceinline__ void cursor_next(const TcParams& prm, TileCursor& c) 
     ++c.pi;
     c.m0 = 0;
     c.n0 = 0;
-    cursor_load(prm, c);
+    cursor_load<BNT>(prm, c);
   }
 }
 
@@ -154,23 +158,32 @@ __device__ __forceinline__ int blk_key(int pi, int m0) { return (pi << 24) | (m0
 // kCheck: compute the non-finite flag (instantiated only when the caller asked for it).
 // kRR: round-robin tile schedule (streaming-A problems), else contiguous ranges.
 // kNorm: x is the raw latent and its RMSNorm is fused (see the epilogue).
-template <bool kBF16, bool kCheck, bool kRR, bool kNorm = false>
+// BNT: tile width, 256 or — for launches too short to give every pair two 256-wide tiles
+// (decode-to-prefill batches on wide problems) — 128: twice the tiles to balance over the
+// pairs, each warp's epilogue one 64-column span, four TMEM accumulator buffers.
+template <bool kBF16, bool kCheck, bool kRR, bool kNorm = false, int BNT = BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     kv_proj_tc_kernel(const __grid_constant__ TcParams prm) {
+  static_assert(BNT == 256 || BNT == 128, "tile width");
+  constexpr int NACC = 512 / BNT;                   // accumulator buffers
+  constexpr int BST = B_STAGES * (BN / BNT);        // B ring stages (same bytes)
+  constexpr int BPAN = (BNT / 64) / CG;             // this CTA's B panels per stage
+  constexpr uint32_t BBYTES = BPAN * B_PANEL;
+  constexpr int NSUB = BNT / 64;                    // 32-column sub-chunks per epilogue warp
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = sA + A_SLOTS * A_BYTES;
-  uint8_t* sRep = sB + B_STAGES * B_BYTES;
+  uint8_t* sRep = sB + B_STAGES * B_BYTES;  // the ring's bytes do not depend on BNT
   uint8_t* sStg = sRep + REP_BYTES;                 // EPI_WARPS x STG_BUFS x STG_BYTES
   uint64_t* a_full = reinterpret_cast<uint64_t*>(sStg + EPI_WARPS * STG_BUFS * STG_BYTES);
   uint64_t* a_empty = a_full + A_SLOTS;
   uint64_t* b_full = a_empty + A_SLOTS;
-  uint64_t* b_empty = b_full + B_STAGES;
-  uint64_t* tfull = b_empty + B_STAGES;
-  uint64_t* tempty = tfull + NUM_ACC;
-  uint64_t* rfull = tempty + NUM_ACC;
+  uint64_t* b_empty = b_full + BST;
+  uint64_t* tfull = b_empty + BST;
+  uint64_t* tempty = tfull + NACC;
+  uint64_t* rfull = tempty + NACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 1);
   float* norm_part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(a_full) + 512);
 
@@ -188,11 +201,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // one multicast tcgen05.commit (+ kNorm: this CTA's epilogue, done reading the slot)
       mbar_init(&a_empty[s], kNorm ? 2 : 1);
     }
-    for (int s = 0; s < B_STAGES; ++s) {
+    for (int s = 0; s < BST; ++s) {
       mbar_init(&b_full[s], 1);
       mbar_init(&b_empty[s], 1);
     }
-    for (int a = 0; a < NUM_ACC; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], CG);  // one arrival per CTA's epilogue (leader's copy)
     }
@@ -249,20 +262,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (t_begin < t_end) {
         // decode the first tile (parameter-cache misses) while the previous grid drains
         int pi, m0, n0;
-        decode_tile(prm, t_begin, pi, m0, n0);
+        decode_tile<BNT>(prm, t_begin, pi, m0, n0);
         const int nkb = prm.p[pi].num_kb;
         asm volatile("" ::"r"(pi), "r"(m0), "r"(n0), "r"(nkb));
       }
       griddep_wait();
       for (int t = t_begin; t < t_end; t += t_step) {
         int pi, m0, n0;
-        decode_tile(prm, t, pi, m0, n0);
+        decode_tile<BNT>(prm, t, pi, m0, n0);
         const TcProblem& P = prm.p[pi];
         const int key = blk_key(pi, m0);
         const bool reload_a = P.num_kb > A_SLOTS || key != prev_key;
         prev_key = key;
         const int my_m0 = m0 + static_cast<int>(rank) * BM;
-        const int my_n0 = n0 + static_cast<int>(rank) * (BN / CG);
+        const int my_n0 = n0 + static_cast<int>(rank) * (BNT / CG);
         for (int j = 0; j < P.num_kbb; ++j) {
           const int kb = j / B_SUB;
           // Both CTAs' bytes complete on the LEADER's barriers, which the leader arms with
@@ -280,14 +293,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             __syncwarp();
             ++a_iter;
           }
-          const uint32_t s = b_iter % B_STAGES;
-          mbar_wait(&b_empty[s], ((b_iter / B_STAGES) & 1u) ^ 1u);
+          const uint32_t s = b_iter % BST;
+          mbar_wait(&b_empty[s], ((b_iter / BST) & 1u) ^ 1u);
           if (elect_one()) {
-            if (rank == 0) mbar_arrive_expect_tx(&b_full[s], CG * B_BYTES);
+            if (rank == 0) mbar_arrive_expect_tx(&b_full[s], CG * BBYTES);
             const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), 0);
 #pragma unroll
-            for (int q = 0; q < B_PANELS; ++q)
-              tma_load_2d_pair(sB + s * B_BYTES + q * B_PANEL, &P.map_b, my_n0 + 64 * q,
+            for (int q = 0; q < BPAN; ++q)
+              tma_load_2d_pair(sB + s * BBYTES + q * B_PANEL, &P.map_b, my_n0 + 64 * q,
                                j * BKB, bar, pol);
           }
           __syncwarp();
@@ -301,13 +314,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // uniform registers); one elected lane issues the tcgen05 instructions.
     if (rank == 0) {
       constexpr uint32_t idesc =
-          make_idesc_f16(kBF16, BM * CG, BN, /*a_mn=*/false, /*b_mn=*/true);
+          make_idesc_f16(kBF16, BM * CG, BNT, /*a_mn=*/false, /*b_mn=*/true);
       uint32_t a_iter = 0, a_base = 0, b_iter = 0;
       int prev_key = -1;
       int it = 0;
-      TileCursor cur = cursor_at(prm, t_begin, t_step);
+      TileCursor cur = cursor_at<BNT>(prm, t_begin, t_step);
       TileCursor nxt = cur;
-      cursor_next<kRR>(prm, nxt);
+      cursor_next<kRR, BNT>(prm, nxt);
       for (int t = t_begin; t < t_end; t += t_step, ++it) {
         const int pi = cur.pi;
         const TcProblem& P = prm.p[pi];
@@ -320,26 +333,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool last_use =
             stream_a || t + t_step >= t_end || blk_key(nxt.pi, nxt.m0) != key;
         cur = nxt;
-        cursor_next<kRR>(prm, nxt);
+        cursor_next<kRR, BNT>(prm, nxt);
         if (reload_a) {
           a_base = a_iter;
           a_iter += num_kb;
         }
-        const int acc = it % NUM_ACC;
-        const uint32_t acc_phase = (it / NUM_ACC) & 1;
+        const int acc = it % NACC;
+        const uint32_t acc_phase = (it / NACC) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * BNT;
         for (int j = 0; j < num_kbb; ++j) {
           const int kb = j / B_SUB;
           const uint32_t ai = a_base + kb;
           const uint32_t as = ai % A_SLOTS;
           if (reload_a && j % B_SUB == 0) mbar_wait(&a_full[as], (ai / A_SLOTS) & 1u);
-          const uint32_t bs = b_iter % B_STAGES;
-          mbar_wait(&b_full[bs], (b_iter / B_STAGES) & 1u);
+          const uint32_t bs = b_iter % BST;
+          mbar_wait(&b_full[bs], (b_iter / BST) & 1u);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + as * A_BYTES);
-          const uint32_t b0 = smem_u32(sB + bs * B_BYTES);
+          const uint32_t b0 = smem_u32(sB + bs * BBYTES);
           if (elect_one()) {
 #pragma unroll
             for (int ks = 0; ks < BKB / UK; ++ks) {
@@ -380,7 +393,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // leader only: stage the rep tile of tile t (this CTA's 128 rows) into the slot
     auto issue_rep = [&](int t) {
       int pi, m0, n0;
-      decode_tile(prm, t, pi, m0, n0);
+      decode_tile<BNT>(prm, t, pi, m0, n0);
       const TcProblem& P = prm.p[pi];
       const int nbox = P.d_h / 64;
       mbar_arrive_expect_tx(rfull, nbox * REP_BOX);
@@ -395,7 +408,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     auto issue_next_rep = [&](int t, int key) {
       for (; t < t_end; t += t_step) {
         int pi, m0, n0;
-        decode_tile(prm, t, pi, m0, n0);
+        decode_tile<BNT>(prm, t, pi, m0, n0);
         if (prm.p[pi].rep_fast && blk_key(pi, m0) != key) {
           issue_rep(t);
           return;
@@ -404,7 +417,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
     if (leader && t_begin < t_end) {
       int pi, m0, n0;
-      decode_tile(prm, t_begin, pi, m0, n0);
+      decode_tile<BNT>(prm, t_begin, pi, m0, n0);
       const int fast0 = prm.p[pi].rep_fast;
       asm volatile("" ::"r"(fast0));
       griddep_wait();
@@ -428,7 +441,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int it = 0;
     for (int t = t_begin; t < t_end; t += t_step, ++it) {
       int pi, m0, n0;
-      decode_tile(prm, t, pi, m0, n0);
+      decode_tile<BNT>(prm, t, pi, m0, n0);
       const TcProblem& P = prm.p[pi];
       const int my_m0 = m0 + static_cast<int>(rank) * BM;
       const int key = blk_key(pi, m0);
@@ -456,8 +469,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         named_bar_sync(2, 32 * EPI_WARPS);  // every epilogue thread holds its rep values
         if (leader) issue_next_rep(t + t_step, key);  // the next fast row-block's rep
       }
-      const int acc = it % NUM_ACC;
-      const uint32_t acc_phase = (it / NUM_ACC) & 1;
+      const int acc = it % NACC;
+      const uint32_t acc_phase = (it / NACC) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if constexpr (kNorm) {
@@ -533,8 +546,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       auto cb = [&](int c) { return (c >> 1) * 128 + static_cast<int>(half) * 64 + (c & 1) * 32; };
       int nsub = 0;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) nsub += (n0 + cb(c) < P.N) ? 1 : 0;
-      const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * BN;
+      for (int c = 0; c < NSUB; ++c) nsub += (n0 + cb(c) < P.N) ? 1 : 0;
+      const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + acc * BNT;
 
       // One 32-column sub-chunk c: + rep, round, swizzled staging into the warp's
       // 32 x 64 box (two sub-chunks per box, one box per span); the box's TMA store is
@@ -625,7 +638,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t ra[32], rb[32];
         tmem_ld_32x32b_x32(taddr + cb(0), ra);
 #pragma unroll
-        for (int c = 0; c < 4; c += 2) {
+        for (int c = 0; c < NSUB; c += 2) {
           if (c < nsub) {
             tmem_ld_wait();
             if (c + 1 < nsub) tmem_ld_32x32b_x32(taddr + cb(c + 1), rb);
@@ -1271,6 +1284,26 @@ int build_params(const Problem* probs, int count, bool bf16, tc::TcParams& prm,
   prm = TcParams{};
   CUtensorMap peer_host[BD_MAX_GROUP * BD_MAX_PEERS];
   prm.count = count;
+  // Tile width: 128 when 256-wide tiles would not give every pair two tiles (short
+  // launches on wide problems: one 256-wide tile per pair serialises its loads, MMAs and
+  // epilogue; 128-wide tiles pipeline them and balance better).  Streaming-A, fused-norm
+  // and fused-all-gather launches keep 256.  BD_TILE_N=128|256 forces a width (A/B).
+  static const int tile_env = [] {
+    const char* e = getenv("BD_TILE_N");
+    return e != nullptr ? atoi(e) : 0;
+  }();
+  int bn = BN;
+  {
+    int64_t t256 = 0;
+    bool plain = true;
+    for (int i = 0; i < count; ++i) {
+      const Problem& q = probs[i];
+      t256 += ((q.N + BN - 1) / BN) * ((q.L + BM * cg - 1) / (BM * cg));
+      plain = plain && q.rep_gamma == nullptr && q.world == 0 && (q.K + BK - 1) / BK <= A_SLOTS;
+    }
+    if (plain && (tile_env == 128 || (tile_env != 256 && t256 < 2 * (sm_count() / cg)))) bn = 128;
+  }
+  prm.bn = bn;
   int total = 0;
   for (int i = 0; i < count; ++i) {
     const Problem& q = probs[i];
@@ -1327,7 +1360,7 @@ int build_params(const Problem* probs, int count, bool bf16, tc::TcParams& prm,
     P.K = static_cast<int32_t>(K);
     P.d_h = static_cast<int32_t>(d_h);
     P.rep_base = static_cast<int32_t>(rep_base);
-    P.tiles_n = static_cast<int32_t>((N + BN - 1) / BN);
+    P.tiles_n = static_cast<int32_t>((N + bn - 1) / bn);
     P.num_kb = static_cast<int32_t>((K + BK - 1) / BK);
     P.num_kbb = static_cast<int32_t>((K + BKB - 1) / BKB);
     P.tile_start = total;
@@ -1371,10 +1404,16 @@ int launch_params(const tc::TcParams& prm, int total, bool bf16, bool check,
   static const KernFn kerns_norm[2][2] = {
       {kv_proj_tc_kernel<false, false, false, true>, kv_proj_tc_kernel<false, true, false, true>},
       {kv_proj_tc_kernel<true, false, false, true>, kv_proj_tc_kernel<true, true, false, true>}};
-  const int vb = bf16 ? 1 : 0, vc = check ? 1 : 0, vr = prm.norm ? 2 : (prm.strided ? 1 : 0);
-  KernFn kern = vr == 2 ? kerns_norm[vb][vc] : kerns[vb][vc][vr];
+  static const KernFn kerns_128[2][2] = {
+      {kv_proj_tc_kernel<false, false, false, false, 128>,
+       kv_proj_tc_kernel<false, true, false, false, 128>},
+      {kv_proj_tc_kernel<true, false, false, false, 128>,
+       kv_proj_tc_kernel<true, true, false, false, 128>}};
+  const int vb = bf16 ? 1 : 0, vc = check ? 1 : 0;
+  const int vr = prm.bn == 128 ? 3 : prm.norm ? 2 : (prm.strided ? 1 : 0);
+  KernFn kern = vr == 3 ? kerns_128[vb][vc] : vr == 2 ? kerns_norm[vb][vc] : kerns[vb][vc][vr];
   const size_t smem = SMEM_BYTES;
-  static std::atomic<bool> attr_set[kMaxDevices][2][2][3] = {};  // per device (see launch_small)
+  static std::atomic<bool> attr_set[kMaxDevices][2][2][4] = {};  // per device (see launch_small)
   static std::mutex attr_mu;
   const int dv = device_slot();
   if (!attr_set[dv][vb][vc][vr].load(std::memory_order_acquire)) {

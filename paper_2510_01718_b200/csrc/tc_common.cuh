@@ -60,6 +60,7 @@ struct TcParams {
   int32_t dk_b_bytes;
   int32_t dk_recv_bytes;
   int32_t small_rblocks;  // small-L kernel: row blocks of BM * CGS rows (grid = cols x rows)
+  int32_t bn;             // persistent kernel: tile width (256, or 128 for short launches)
 };
 
 template <bool kBF16>

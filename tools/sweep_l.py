@@ -22,7 +22,7 @@ for L in Ls:
 
     def step():
         bd.fused_kv_proj_grouped(x, [(ck, d_h, n, bd.Tag.FIRST), (cv, d_h, n, bd.Tag.LAST)],
-                                 outs=[k, v])
+                                 outs=[k, v], check_finite=False)
 
     for _ in range(5):
         step()
