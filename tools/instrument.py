@@ -66,8 +66,8 @@ rep('''        mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         if (lane == 0 && it < 8) TL[8 + it] = CK();
         unsigned long long bw = 0;''')
-rep('''          mbar_wait(&b_full[bs], (b_iter / B_STAGES) & 1u);''', '''          const unsigned long long w0 = CK();
-          mbar_wait(&b_full[bs], (b_iter / B_STAGES) & 1u);
+rep('''          mbar_wait(&b_full[bs], (b_iter / BST) & 1u);''', '''          const unsigned long long w0 = CK();
+          mbar_wait(&b_full[bs], (b_iter / BST) & 1u);
           bw += CK() - w0;''')
 for m in ("0x3", "pmask"):
     a = f'''        if (elect_one()) tc_commit_pair(&tfull[acc], {m});
