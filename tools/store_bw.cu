@@ -5,6 +5,7 @@
 //   mode 0: st.global.v4 from registers (coalesced rows)
 //   mode 1: 1-D bulk stores smem -> global (cp.async.bulk, 16 KB each, 4 in flight)
 //   mode 2: mode 1 + bulk loads L2 -> smem of `ld_ratio` bytes per stored byte
+// Grids of 16..148 CTAs separate a per-SM store limit from the memory system's.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/sb tools/store_bw.cu
 #include <cuda_runtime.h>
 #include <cstdio>
@@ -72,14 +73,16 @@ int main() {
   uint8_t* src;
   cudaMalloc(&src, S);
   cudaMemset(src, 1, S);
-  struct V { int mode; float ratio; };
-  for (V v : {V{0, 0.f}, V{1, 0.f}, V{2, 1.0f}, V{2, 1.5f}, V{2, 2.0f}}) {
+  struct V { int mode; float ratio; int grid; };
+  for (V v : {V{0, 0.f, 148}, V{1, 0.f, 148}, V{2, 1.0f, 148}, V{2, 1.5f, 148}, V{2, 2.0f, 148},
+              V{1, 0.f, 16}, V{1, 0.f, 37}, V{1, 0.f, 74}, V{0, 0.f, 16}, V{0, 0.f, 74},
+              V{2, 2.0f, 16}, V{2, 2.0f, 74}}) {
     cudaGraph_t g;
     cudaGraphExec_t ge;
     const int inner = 30;
     cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal);
     for (int i = 0; i < inner; ++i)
-      k_store<<<148, 256, 131072, s>>>(dst[i % R], W, src, S, v.mode, v.ratio);
+      k_store<<<v.grid, 256, 131072, s>>>(dst[i % R], W, src, S, v.mode, v.ratio);
     cudaStreamEndCapture(s, &g);
     cudaGraphInstantiate(&ge, g, 0);
     cudaGraphLaunch(ge, s);
@@ -98,9 +101,10 @@ int main() {
       best = ms < best ? ms : best;
     }
     const double us = best * 1000 / inner;
-    printf("mode %d ld_ratio %.1f: %7.2f us per 64 MB written -> %6.0f GB/s stores (+ %6.0f GB/s L2 loads)  %s\n",
-           v.mode, v.ratio, us, W / us / 1e3, v.mode == 2 ? W * v.ratio / us / 1e3 : 0.0,
-           cudaGetErrorString(cudaGetLastError()));
+    printf("mode %d ld_ratio %.1f grid %3d: %7.2f us per 64 MB written -> %6.0f GB/s stores "
+           "(%5.1f GB/s per SM) (+ %6.0f GB/s L2 loads)  %s\n",
+           v.mode, v.ratio, v.grid, us, W / us / 1e3, W / us / 1e3 / v.grid,
+           v.mode == 2 ? W * v.ratio / us / 1e3 : 0.0, cudaGetErrorString(cudaGetLastError()));
     cudaGraphExecDestroy(ge);
     cudaGraphDestroy(g);
   }
