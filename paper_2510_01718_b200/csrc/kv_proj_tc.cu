@@ -39,7 +39,8 @@
 // Tile schedule: contiguous ranges per pair (A residency), or round-robin when A
 // streams (K > 384: keeps the live A/C set inside L2 — cfg3 0.74x -> 1.00x cuBLAS).
 // Variants: kCheck (non-finite flag), kRR (round-robin), kNorm (RMSNorm of x fused:
-// the epilogue sums each row's squares from the resident A slots + rep registers).
+// the epilogue sums each row's squares from the resident A slots + rep registers), BNT
+// (tile width: 256, or 128 for launches too short to give every pair two 256-wide tiles).
 // Also in this file: kv_proj_small_kernel, the L <= 128 (decode) path — one CTA per
 // column block, every k-block loaded at once, cta_group::1 — and the host launchers
 // with their launch-parameter cache.
