@@ -793,6 +793,14 @@ def _run_gather(args, bd, torch, dist, dev, rank, world, dtype, P, d, d_h, n_tot
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item()) * 1e3
 
+    def all_ok(ok: bool) -> bool:
+        """Every rank agrees before a timed collective loop: a rank that failed locally
+        must not leave the others blocked in a barrier (the multi-GPU paths have only run
+        on one device here, so they are guarded rather than trusted)."""
+        t = torch.tensor([1 if ok else 0], device=dev, dtype=torch.int32)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item())
+
     modes = ["nccl", "fused"] if args.gather == "both" else [args.gather]
     if "nccl" in modes:
         def nccl_step():
@@ -800,14 +808,27 @@ def _run_gather(args, bd, torch, dist, dev, rank, world, dtype, P, d, d_h, n_tot
             P.all_gather_heads(kh, d_h)
             P.all_gather_heads(vh, d_h)
         try:
+            if not all_ok(True):
+                raise RuntimeError("a rank could not start the NCCL gather")
             us = time_eager(nccl_step)
             out["nccl"] = {"us": round(us, 2), "tokens_per_s": L * world / (us * 1e-6),
                            "what": "projection (head-major) + NCCL all_gather_into_tensor x2"}
         except Exception as exc:  # report, never hide
             out["nccl"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if "fused" in modes:
+        sg, local_err = None, None
         try:
             sg = P.SymmetricGather([(n_total, L, d_h), (n_total, L, d_h)], dtype)
+            # one un-timed projection with the fused gather (no barrier yet): a launch
+            # error shows up here, on this rank, before any rank enters a collective
+            P.fused_allgather_kv_proj(x, specs, sg.peers, sg.rank)
+            torch.cuda.synchronize()
+        except Exception as exc:
+            local_err = f"{type(exc).__name__}: {exc}"[:300]
+        try:
+            if not all_ok(local_err is None):
+                raise RuntimeError(local_err or "another rank could not set up the fused gather")
+            sg.barrier()
 
             def fused_step():
                 P.fused_allgather_kv_proj(x, specs, sg.peers, sg.rank)
