@@ -5,6 +5,7 @@ test_cli.py:98-128): the reference columns first, in order, then the GPU columns
 import csv
 
 import pytest
+from conftest import ROOT
 import torch
 
 from paper_2510_01718_b200 import benchmark as B
@@ -37,3 +38,24 @@ def test_record_row_and_csv(tmp_path):
                       inner_calls=1)
     with pytest.raises(ValueError):
         B.time_operator_ns(lambda: None, reps=4)
+
+
+def test_reference_arm_prints_one_contract_line():
+    """`bench.py --impl reference` (the driver's reference arm) runs the oracle port on the
+    host cores and prints ONE JSON line with the contract's keys, on this CPU-only box."""
+    import json
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                          "--steps", "2", "--warmup", "1", "--tokens", "256"],
+                         capture_output=True, text=True, timeout=300, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "cpu_baseline", "e2e"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
