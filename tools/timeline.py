@@ -75,3 +75,22 @@ if tl.shape[1] > 64 and (tl[full, 64] > 0).any():
         print(f"epilogue tile 3, {name}: tfull-wait-done {m[12]}, first-ld {m[1]} |",
               "after chunk c: ", [m[2], m[4], m[6], m[8]], "| loads ready c=1..3:", [m[3], m[5], m[7]],
               "| loop end", m[9], "| barrier done", m[10])
+
+# straddling: does the pair's contiguous tile range cross a (problem, row-block) boundary
+# (16 tiles per row-block per problem at cfg2) — i.e. load A twice?
+if not single and L == 8192 and n == 16:
+    units = 74
+    tot = 512
+    lead_all = np.arange(0, 148, 2)
+    ends = tl[lead_all, 41] - g0
+    rows = []
+    for u in range(units):
+        tb, te = u * tot // units, (u + 1) * tot // units
+        rows.append((te - tb, int(tb // 16 != (te - 1) // 16), int(ends[u])))
+    arr = np.array(rows)
+    for nt in (6, 7):
+        for st in (0, 1):
+            sel = (arr[:, 0] == nt) & (arr[:, 1] == st)
+            if sel.any():
+                print(f"tiles={nt} straddle={st}: pairs {sel.sum():2d}, end ns median "
+                      f"{int(np.median(arr[sel, 2]))}, max {int(arr[sel, 2].max())}")
