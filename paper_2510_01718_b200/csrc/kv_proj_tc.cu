@@ -40,7 +40,8 @@
 // streams (K > 384: keeps the live A/C set inside L2 — cfg3 0.74x -> 1.00x cuBLAS).
 // Variants: kCheck (non-finite flag), kRR (round-robin), kNorm (RMSNorm of x fused:
 // the epilogue sums each row's squares from the resident A slots + rep registers), BNT
-// (tile width: 256, or 128 for launches too short to give every pair two 256-wide tiles).
+// (tile width: 256, or 128 for launches too short to give every pair two 256-wide tiles),
+// kSwap (mirror schedule for problems one column tile wide: coefficients resident).
 // Also in this file: kv_proj_small_kernel, the L <= 128 (decode) path — one CTA per
 // column block, every k-block loaded at once, cta_group::1 — and the host launchers
 // with their launch-parameter cache.
@@ -94,14 +95,22 @@ constexpr size_t SMEM_BYTES = 1024 + A_SLOTS * A_BYTES + B_STAGES * B_BYTES + RE
 static_assert((2 * A_SLOTS + 2 * 2 * B_STAGES + 2 * 2 * NUM_ACC + 1) * 8 + 4 <= 512, "barrier area");
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
-template <int BNT = BN>
+// Tile order inside a problem: row-block major (column tiles innermost: consecutive
+// tiles share the A row-block) — or, for the mirror schedule (kSwap), column-tile major
+// (row-blocks innermost: consecutive tiles share the coefficient tile).
+template <int BNT = BN, bool kSwap = false>
 __device__ __forceinline__ void decode_tile(const TcParams& prm, int t, int& pi, int& m0,
                                             int& n0) {
   pi = 0;
   while (pi + 1 < prm.count && t >= prm.p[pi + 1].tile_start) ++pi;
   const int local = t - prm.p[pi].tile_start;
-  n0 = (local % prm.p[pi].tiles_n) * BNT;
-  m0 = (local / prm.p[pi].tiles_n) * (BM * CG);
+  if constexpr (kSwap) {
+    m0 = (local % prm.p[pi].tiles_m) * (BM * CG);
+    n0 = (local / prm.p[pi].tiles_m) * BNT;
+  } else {
+    n0 = (local % prm.p[pi].tiles_n) * BNT;
+    m0 = (local / prm.p[pi].tiles_n) * (BM * CG);
+  }
 }
 
 // Sequential walk over a pair's contiguous tile range without per-tile divisions
@@ -110,51 +119,64 @@ __device__ __forceinline__ void decode_tile(const TcParams& prm, int t, int& pi,
 // division + indexed parameter loads) cost ~700 clocks per tile.
 struct TileCursor {
   int pi, m0, n0;
-  int n_span;    // tiles_n * BNT of problem pi
+  int n_span;    // tiles_n * BNT of problem pi (kSwap: tiles_m * BM * CG, the inner loop)
   int pend;      // first tile of problem pi + 1
   int t;
   int step;      // tile stride between this pair's consecutive tiles (1: contiguous)
 };
-template <int BNT>
+template <int BNT, bool kSwap = false>
 __device__ __forceinline__ void cursor_load(const TcParams& prm, TileCursor& c) {
-  c.n_span = prm.p[c.pi].tiles_n * BNT;
+  c.n_span = kSwap ? prm.p[c.pi].tiles_m * (BM * CG) : prm.p[c.pi].tiles_n * BNT;
   c.pend = c.pi + 1 < prm.count ? prm.p[c.pi + 1].tile_start : 0x7fffffff;
 }
-template <int BNT>
+template <int BNT, bool kSwap = false>
 __device__ __forceinline__ TileCursor cursor_at(const TcParams& prm, int t, int step) {
   TileCursor c;
   c.t = t;
   c.step = step;
-  decode_tile<BNT>(prm, t, c.pi, c.m0, c.n0);
-  cursor_load<BNT>(prm, c);
+  decode_tile<BNT, kSwap>(prm, t, c.pi, c.m0, c.n0);
+  cursor_load<BNT, kSwap>(prm, c);
   return c;
 }
-template <bool kRR, int BNT>
+template <bool kRR, int BNT, bool kSwap = false>
 __device__ __forceinline__ void cursor_next(const TcParams& prm, TileCursor& c) {
   if constexpr (kRR) {  // round-robin tiles (long K): a full decode is off the critical path
     c.t += c.step;
     if (c.t < prm.total_tiles) {
-      decode_tile<BNT>(prm, c.t, c.pi, c.m0, c.n0);
-      cursor_load<BNT>(prm, c);
+      decode_tile<BNT, kSwap>(prm, c.t, c.pi, c.m0, c.n0);
+      cursor_load<BNT, kSwap>(prm, c);
     }
     return;
   }
   ++c.t;
-  c.n0 += BNT;
-  if (c.n0 >= c.n_span) {
-    c.n0 = 0;
+  if constexpr (kSwap) {
     c.m0 += BM * CG;
+    if (c.m0 >= c.n_span) {
+      c.m0 = 0;
+      c.n0 += BNT;
+    }
+  } else {
+    c.n0 += BNT;
+    if (c.n0 >= c.n_span) {
+      c.n0 = 0;
+      c.m0 += BM * CG;
+    }
   }
   if (c.t >= c.pend) {
     ++c.pi;
     c.m0 = 0;
     c.n0 = 0;
-    cursor_load<BNT>(prm, c);
+    cursor_load<BNT, kSwap>(prm, c);
   }
 }
 
 // Tiles sharing (problem, pair row-block) share the A row-block and the rep tile.
 __device__ __forceinline__ int blk_key(int pi, int m0) { return (pi << 24) | (m0 / (BM * CG)); }
+// The resident operand's key: the A row-block, or (kSwap) the coefficient column tile.
+template <bool kSwap, int BNT>
+__device__ __forceinline__ int res_key(int pi, int m0, int n0) {
+  return kSwap ? ((pi << 24) | (n0 / BNT)) : blk_key(pi, m0);
+}
 
 // kCheck: compute the non-finite flag (instantiated only when the caller asked for it).
 // kRR: round-robin tile schedule (streaming-A problems), else contiguous ranges.
@@ -162,10 +184,18 @@ __device__ __forceinline__ int blk_key(int pi, int m0) { return (pi << 24) | (m0
 // BNT: tile width, 256 or — for launches too short to give every pair two 256-wide tiles
 // (decode-to-prefill batches on wide problems) — 128: twice the tiles to balance over the
 // pairs, each warp's epilogue one 64-column span, four TMEM accumulator buffers.
-template <bool kBF16, bool kCheck, bool kRR, bool kNorm = false, int BNT = BN>
+// kSwap: the mirror schedule for narrow problems (a problem one or two column tiles wide,
+// e.g. 2 + 2 heads per GPU under head sharding): the coefficient tile is the RESIDENT
+// operand (six 16 KiB slots hold this CTA's 128 columns x K) and x streams through the
+// ring, tiles ordered column-tile major — consecutive tiles reuse the coefficients
+// instead of reloading a 96 KiB A row-block per tile.  Same MMAs, same k order: outputs
+// are bit-identical to the row-block-major schedule's.
+template <bool kBF16, bool kCheck, bool kRR, bool kNorm = false, int BNT = BN, bool kSwap = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     kv_proj_tc_kernel(const __grid_constant__ TcParams prm) {
   static_assert(BNT == 256 || BNT == 128, "tile width");
+  static_assert(!kSwap || (BNT == 256 && !kRR && !kNorm && B_SUB == 1),
+                "mirror schedule: 256-wide tiles, resident K <= 384, no fused norm");
   constexpr int NACC = 512 / BNT;                   // accumulator buffers
   constexpr int BST = B_STAGES * (BN / BNT);        // B ring stages (same bytes)
   constexpr int BPAN = (BNT / 64) / CG;             // this CTA's B panels per stage
@@ -263,17 +293,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (t_begin < t_end) {
         // decode the first tile (parameter-cache misses) while the previous grid drains
         int pi, m0, n0;
-        decode_tile<BNT>(prm, t_begin, pi, m0, n0);
+        decode_tile<BNT, kSwap>(prm, t_begin, pi, m0, n0);
         const int nkb = prm.p[pi].num_kb;
         asm volatile("" ::"r"(pi), "r"(m0), "r"(n0), "r"(nkb));
       }
       griddep_wait();
       for (int t = t_begin; t < t_end; t += t_step) {
         int pi, m0, n0;
-        decode_tile<BNT>(prm, t, pi, m0, n0);
+        decode_tile<BNT, kSwap>(prm, t, pi, m0, n0);
         const TcProblem& P = prm.p[pi];
-        const int key = blk_key(pi, m0);
-        const bool reload_a = P.num_kb > A_SLOTS || key != prev_key;
+        const int key = res_key<kSwap, BNT>(pi, m0, n0);
+        const bool reload_a = P.num_kb > A_SLOTS || key != prev_key;  // the resident operand
         prev_key = key;
         const int my_m0 = m0 + static_cast<int>(rank) * BM;
         const int my_n0 = n0 + static_cast<int>(rank) * (BNT / CG);
@@ -288,8 +318,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_wait(&a_empty[s], ((a_iter / A_SLOTS) & 1u) ^ 1u);
             if (elect_one()) {
               if (rank == 0) mbar_arrive_expect_tx(&a_full[s], CG * A_BYTES);
-              tma_load_2d_pair(sA + s * A_BYTES, &P.map_a, kb * BK, my_m0,
-                               mapa_shared(smem_u32(&a_full[s]), 0), pol);
+              if constexpr (kSwap) {  // this CTA's 128 coefficient columns, k-block kb
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                  tma_load_2d_pair(sA + s * A_BYTES + q * B_PANEL, &P.map_b, my_n0 + 64 * q,
+                                   kb * BK, mapa_shared(smem_u32(&a_full[s]), 0), pol);
+              } else {
+                tma_load_2d_pair(sA + s * A_BYTES, &P.map_a, kb * BK, my_m0,
+                                 mapa_shared(smem_u32(&a_full[s]), 0), pol);
+              }
             }
             __syncwarp();
             ++a_iter;
@@ -299,10 +336,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (elect_one()) {
             if (rank == 0) mbar_arrive_expect_tx(&b_full[s], CG * BBYTES);
             const uint32_t bar = mapa_shared(smem_u32(&b_full[s]), 0);
+            if constexpr (kSwap) {  // this CTA's 128 rows of x, k-block j
+              tma_load_2d_pair(sB + s * BBYTES, &P.map_a, j * BKB, my_m0, bar, pol);
+            } else {
 #pragma unroll
-            for (int q = 0; q < BPAN; ++q)
-              tma_load_2d_pair(sB + s * BBYTES + q * B_PANEL, &P.map_b, my_n0 + 64 * q,
-                               j * BKB, bar, pol);
+              for (int q = 0; q < BPAN; ++q)
+                tma_load_2d_pair(sB + s * BBYTES + q * B_PANEL, &P.map_b, my_n0 + 64 * q,
+                                 j * BKB, bar, pol);
+            }
           }
           __syncwarp();
           ++b_iter;
@@ -319,22 +360,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t a_iter = 0, a_base = 0, b_iter = 0;
       int prev_key = -1;
       int it = 0;
-      TileCursor cur = cursor_at<BNT>(prm, t_begin, t_step);
+      TileCursor cur = cursor_at<BNT, kSwap>(prm, t_begin, t_step);
       TileCursor nxt = cur;
-      cursor_next<kRR, BNT>(prm, nxt);
+      cursor_next<kRR, BNT, kSwap>(prm, nxt);
       for (int t = t_begin; t < t_end; t += t_step, ++it) {
         const int pi = cur.pi;
         const TcProblem& P = prm.p[pi];
         const int num_kb = P.num_kb, num_kbb = P.num_kbb;
-        const int key = blk_key(pi, cur.m0);
+        const int key = res_key<kSwap, BNT>(pi, cur.m0, cur.n0);
         const bool stream_a = num_kb > A_SLOTS;
         const bool reload_a = stream_a || key != prev_key;
         prev_key = key;
-        // Last tile reading this A row-block: release each slot after its k-block's MMAs.
-        const bool last_use =
-            stream_a || t + t_step >= t_end || blk_key(nxt.pi, nxt.m0) != key;
+        // Last tile reading this resident block: release each slot after its k-block's MMAs.
+        const bool last_use = stream_a || t + t_step >= t_end ||
+                              res_key<kSwap, BNT>(nxt.pi, nxt.m0, nxt.n0) != key;
         cur = nxt;
-        cursor_next<kRR, BNT>(prm, nxt);
+        cursor_next<kRR, BNT, kSwap>(prm, nxt);
         if (reload_a) {
           a_base = a_iter;
           a_iter += num_kb;
@@ -359,11 +400,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int ks = 0; ks < BKB / UK; ++ks) {
               // A: K-major SW128, rows 128 B apart, 8-row groups 1024 B apart; a 16-wide
               //    k step is +32 B inside the swizzle row.
+              // (kSwap: the same two layouts with the regions exchanged — x's k-block in
+              //  the ring stage, the coefficient panels in the resident slot)
+              const uint32_t abase = kSwap ? b0 : a0;
+              const uint32_t bbase = kSwap ? a0 : b0;
               const uint64_t adesc =
-                  make_smem_desc(a0 + ((j % B_SUB) * BKB + ks * UK) * 2, 16, 1024);
+                  make_smem_desc(abase + ((j % B_SUB) * BKB + ks * UK) * 2, 16, 1024);
               // B: MN-major SW128, 64-column panels B_PANEL apart (LBO), 8-k-row groups
               //    1024 B apart (SBO); a 16-deep k step is two 8-row groups = 2048 B.
-              const uint64_t bdesc = make_smem_desc(b0 + ks * (UK * 128), B_PANEL, 1024);
+              const uint64_t bdesc = make_smem_desc(bbase + ks * (UK * 128), B_PANEL, 1024);
               tc_mma_f16_pair(d_tmem, adesc, bdesc, idesc, (j | ks) != 0 ? 1u : 0u);
             }
             tc_commit_pair(&b_empty[bs], 0x3);
@@ -394,7 +439,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // leader only: stage the rep tile of tile t (this CTA's 128 rows) into the slot
     auto issue_rep = [&](int t) {
       int pi, m0, n0;
-      decode_tile<BNT>(prm, t, pi, m0, n0);
+      decode_tile<BNT, kSwap>(prm, t, pi, m0, n0);
       const TcProblem& P = prm.p[pi];
       const int nbox = P.d_h / 64;
       mbar_arrive_expect_tx(rfull, nbox * REP_BOX);
@@ -409,7 +454,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     auto issue_next_rep = [&](int t, int key) {
       for (; t < t_end; t += t_step) {
         int pi, m0, n0;
-        decode_tile<BNT>(prm, t, pi, m0, n0);
+        decode_tile<BNT, kSwap>(prm, t, pi, m0, n0);
         if (prm.p[pi].rep_fast && blk_key(pi, m0) != key) {
           issue_rep(t);
           return;
@@ -418,7 +463,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
     if (leader && t_begin < t_end) {
       int pi, m0, n0;
-      decode_tile<BNT>(prm, t_begin, pi, m0, n0);
+      decode_tile<BNT, kSwap>(prm, t_begin, pi, m0, n0);
       const int fast0 = prm.p[pi].rep_fast;
       asm volatile("" ::"r"(fast0));
       griddep_wait();
@@ -442,7 +487,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int it = 0;
     for (int t = t_begin; t < t_end; t += t_step, ++it) {
       int pi, m0, n0;
-      decode_tile<BNT>(prm, t, pi, m0, n0);
+      decode_tile<BNT, kSwap>(prm, t, pi, m0, n0);
       const TcProblem& P = prm.p[pi];
       const int my_m0 = m0 + static_cast<int>(rank) * BM;
       const int key = blk_key(pi, m0);
@@ -1362,6 +1407,7 @@ int build_params(const Problem* probs, int count, bool bf16, tc::TcParams& prm,
     P.d_h = static_cast<int32_t>(d_h);
     P.rep_base = static_cast<int32_t>(rep_base);
     P.tiles_n = static_cast<int32_t>((N + bn - 1) / bn);
+    P.tiles_m = static_cast<int32_t>((q.L + BM * cg - 1) / (BM * cg));
     P.num_kb = static_cast<int32_t>((K + BK - 1) / BK);
     P.num_kbb = static_cast<int32_t>((K + BKB - 1) / BKB);
     P.tile_start = total;
@@ -1370,6 +1416,20 @@ int build_params(const Problem* probs, int count, bool bf16, tc::TcParams& prm,
   prm.total_tiles = total;
   for (int i = 0; i < count; ++i)
     if (prm.p[i].num_kb > A_SLOTS) prm.strided = 1;
+  // Mirror schedule (coefficients resident, x streamed) when every problem is a single
+  // 256-wide column tile: the row-block-major schedule would reload a 96 KiB A
+  // row-block for every tile (head-sharded weak scaling at 2 + 2 heads per GPU).
+  // BD_SWAP=0|1 forces it off / on where legal (A/B).
+  {
+    static const int swap_env = [] {
+      const char* e = getenv("BD_SWAP");
+      return e != nullptr ? atoi(e) : -1;
+    }();
+    bool legal = bn == BN && !prm.strided && !prm.norm && prm.world == 0;
+    bool narrow = true;
+    for (int i = 0; i < count; ++i) narrow = narrow && prm.p[i].tiles_n == 1;
+    prm.swap = legal && (swap_env == 1 || (swap_env != 0 && narrow)) ? 1 : 0;
+  }
   if (prm.world > 0) {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(stream, &cap);
@@ -1405,16 +1465,24 @@ int launch_params(const tc::TcParams& prm, int total, bool bf16, bool check,
   static const KernFn kerns_norm[2][2] = {
       {kv_proj_tc_kernel<false, false, false, true>, kv_proj_tc_kernel<false, true, false, true>},
       {kv_proj_tc_kernel<true, false, false, true>, kv_proj_tc_kernel<true, true, false, true>}};
+  static const KernFn kerns_swap[2][2] = {
+      {kv_proj_tc_kernel<false, false, false, false, BN, true>,
+       kv_proj_tc_kernel<false, true, false, false, BN, true>},
+      {kv_proj_tc_kernel<true, false, false, false, BN, true>,
+       kv_proj_tc_kernel<true, true, false, false, BN, true>}};
   static const KernFn kerns_128[2][2] = {
       {kv_proj_tc_kernel<false, false, false, false, 128>,
        kv_proj_tc_kernel<false, true, false, false, 128>},
       {kv_proj_tc_kernel<true, false, false, false, 128>,
        kv_proj_tc_kernel<true, true, false, false, 128>}};
   const int vb = bf16 ? 1 : 0, vc = check ? 1 : 0;
-  const int vr = prm.bn == 128 ? 3 : prm.norm ? 2 : (prm.strided ? 1 : 0);
-  KernFn kern = vr == 3 ? kerns_128[vb][vc] : vr == 2 ? kerns_norm[vb][vc] : kerns[vb][vc][vr];
+  const int vr = prm.swap ? 4 : prm.bn == 128 ? 3 : prm.norm ? 2 : (prm.strided ? 1 : 0);
+  KernFn kern = vr == 4   ? kerns_swap[vb][vc]
+                : vr == 3 ? kerns_128[vb][vc]
+                : vr == 2 ? kerns_norm[vb][vc]
+                          : kerns[vb][vc][vr];
   const size_t smem = SMEM_BYTES;
-  static std::atomic<bool> attr_set[kMaxDevices][2][2][4] = {};  // per device (see launch_small)
+  static std::atomic<bool> attr_set[kMaxDevices][2][2][5] = {};  // per device (see launch_small)
   static std::mutex attr_mu;
   const int dv = device_slot();
   if (!attr_set[dv][vb][vc][vr].load(std::memory_order_acquire)) {

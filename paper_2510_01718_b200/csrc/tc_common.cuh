@@ -27,6 +27,7 @@ struct TcProblem {
   int64_t ldx;
   int32_t L, N, K, d_h, rep_base;
   int32_t tiles_n, num_kb, num_kbb, tile_start;  // num_kbb: B k-blocks (BKB deep)
+  int32_t tiles_m;      // persistent kernel: pair row-blocks (the mirror schedule's inner loop)
   int32_t has_rep;      // 0: plain GEMM (no repeated-slice add)
   int32_t rep_fast;     // d_h in {64, 128}: rep tile staged in smem by TMA
   int32_t head_major;   // output layout [n_heads][L][d_h]
@@ -61,6 +62,7 @@ struct TcParams {
   int32_t dk_recv_bytes;
   int32_t small_rblocks;  // small-L kernel: row blocks of BM * CGS rows (grid = cols x rows)
   int32_t bn;             // persistent kernel: tile width (256, or 128 for short launches)
+  int32_t swap;           // persistent kernel: mirror schedule (coefficient tile resident)
 };
 
 template <bool kBF16>

@@ -557,3 +557,28 @@ def test_check_finite_is_the_default_like_the_reference(cuda):
         bd.fused_kv_proj_grouped(x, [(c, 32, 2, bd.Tag.FIRST)])
     out = bd.fused_kv_proj_grouped(x, [(c, 32, 2, bd.Tag.FIRST)], check_finite=False)
     assert not bool(torch.isfinite(out[0]).all())
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_mirror_schedule_narrow_shards(dtype, cuda):
+    """2 + 2 heads (one 256-wide column tile per problem) at 20480 tokens: the launch takes
+    the mirror schedule (coefficient tile resident, x streamed, tiles column-tile major).
+    Its outputs equal, bit for bit, the same heads' columns of a 16-head launch (the
+    row-block-major schedule), and one row of every 256-row block meets the FP64 oracle's
+    elementwise bound — the per-rank shape of head-sharded weak scaling at 8 GPUs."""
+    L, d, d_h, n_full, h0, n = 20480, 512, 128, 16, 6, 2
+    g = torch.Generator().manual_seed(88)
+    x = torch.randn(L, d, generator=g).to(dtype).to(cuda)
+    ck = (torch.randn(d - d_h, n_full * d_h, generator=g) / 8).to(dtype).to(cuda)
+    cv = (torch.randn(d - d_h, n_full * d_h, generator=g) / 8).to(dtype).to(cuda)
+    k_full, v_full = bd.fused_kv_proj_grouped(
+        x, [(ck, d_h, n_full, bd.Tag.FIRST), (cv, d_h, n_full, bd.Tag.LAST)], check_finite=False)
+    cols = slice(h0 * d_h, (h0 + n) * d_h)
+    cks, cvs = ck[:, cols].contiguous(), cv[:, cols].contiguous()
+    k, v = bd.fused_kv_proj_grouped(x, [(cks, d_h, n, bd.Tag.FIRST), (cvs, d_h, n, bd.Tag.LAST)],
+                                    check_finite=True)
+    torch.testing.assert_close(k, k_full[:, cols], rtol=0, atol=0)
+    torch.testing.assert_close(v, v_full[:, cols], rtol=0, atol=0)
+    rows = torch.tensor(sorted({min(L - 1, b * 256 + (37 * b) % 256) for b in range(L // 256)}))
+    assert_tc_close(k, x, cks, d_h, n, bd.Tag.FIRST, rows=rows.to(cuda))
+    assert_tc_close(v, x, cvs, d_h, n, bd.Tag.LAST, rows=rows.to(cuda))
