@@ -582,3 +582,30 @@ def test_mirror_schedule_narrow_shards(dtype, cuda):
     rows = torch.tensor(sorted({min(L - 1, b * 256 + (37 * b) % 256) for b in range(L // 256)}))
     assert_tc_close(k, x, cks, d_h, n, bd.Tag.FIRST, rows=rows.to(cuda))
     assert_tc_close(v, x, cvs, d_h, n, bd.Tag.LAST, rows=rows.to(cuda))
+
+
+@pytest.mark.parametrize("layout", ["token", "head"])
+def test_mirror_schedule_k_tail_and_layouts(layout, cuda):
+    """The mirror schedule with a K that is not a multiple of 64 (d = 328, d_h = 64:
+    K = 264, the last coefficient / x k-block zero-filled by TMA), 4 heads of 64 (one
+    256-wide tile) at 20480 tokens, token- and head-major output: equal to the same heads'
+    columns of a 12-head launch (row-block-major) and within the oracle bound."""
+    L, d, d_h, n_full, h0, n = 20480, 328, 64, 12, 4, 4
+    g = torch.Generator().manual_seed(99)
+    x = torch.randn(L, d, generator=g).half().to(cuda)
+    ck = (torch.randn(d - d_h, n_full * d_h, generator=g) / 8).half().to(cuda)
+    cv = (torch.randn(d - d_h, n_full * d_h, generator=g) / 8).half().to(cuda)
+    cols = slice(h0 * d_h, (h0 + n) * d_h)
+    k_full, v_full = bd.fused_kv_proj_grouped(
+        x, [(ck, d_h, n_full, bd.Tag.FIRST), (cv, d_h, n_full, bd.Tag.LAST)], check_finite=False)
+    cks, cvs = ck[:, cols].contiguous(), cv[:, cols].contiguous()
+    k, v = bd.fused_kv_proj_grouped(x, [(cks, d_h, n, bd.Tag.FIRST), (cvs, d_h, n, bd.Tag.LAST)],
+                                    out_layout=layout, check_finite=True)
+    if layout == "head":
+        k = k.transpose(0, 1).reshape(L, n * d_h)
+        v = v.transpose(0, 1).reshape(L, n * d_h)
+    torch.testing.assert_close(k, k_full[:, cols], rtol=0, atol=0)
+    torch.testing.assert_close(v, v_full[:, cols], rtol=0, atol=0)
+    rows = torch.tensor(sorted({min(L - 1, b * 256 + (53 * b) % 256) for b in range(L // 256)}))
+    assert_tc_close(k, x, cks, d_h, n, bd.Tag.FIRST, rows=rows.to(cuda))
+    assert_tc_close(v, x, cvs, d_h, n, bd.Tag.LAST, rows=rows.to(cuda))
