@@ -1140,6 +1140,11 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     // 128 (C streams through as many SMs as possible in a single wave)
     const int per_sm64 = small_smem_bytes(64, a_kb_bytes, false) * 2 <= 232448 ? 2 : 1;
     bns = (cols + 63) / 64 <= static_cast<int64_t>(per_sm64) * sm_count() ? 64 : 128;
+    static const int bns_env = [] {  // BD_SMALL_BNS=64|128: force the column block (A/B)
+      const char* e = getenv("BD_SMALL_BNS");
+      return e != nullptr ? atoi(e) : 0;
+    }();
+    if (bns_env == 64 || bns_env == 128) bns = bns_env;
   } else {
     // pairs: one CTA per SM (A is 96 KiB); 256-column blocks once they fill a wave
     bns = (cols + 127) / 128 * nrb <= static_cast<int64_t>(sm_count() / 2) ? 128 : 256;
