@@ -97,6 +97,28 @@ def test_exact_kernel_matches_oracle_random_shapes(dtype, shape, cuda):
                                       O.fused_kv_proj_ref(x, c, d_h, n, tag.value, threads=8))
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("layout", ["token", "head"])
+@pytest.mark.parametrize("shape", [(4000, 374, 73, 9), (6000, 103, 100, 6)])
+def test_exact_large_tile_path_ragged(dtype, layout, shape, cuda):
+    """Outputs big enough for the 128 x 128 exact tiles (>= 2 tiles per SM), every edge
+    ragged (L, N and K = d - d_h not multiples of the tile or the k-slab; K = 3 is all
+    tail): grouped K'+V', bit-identical to the C restatement of the reference kernel."""
+    L, d, d_h, n = shape
+    rng = O.Rng(sum(shape))
+    x = O.rand_gaussian(rng, L, d, dtype)
+    cs = [O.rand_gaussian(rng, d - d_h, n * d_h, dtype) for _ in range(2)]
+    xt = torch.from_numpy(x).to(cuda)
+    specs = [(torch.from_numpy(c).to(cuda), d_h, n, t) for c, t in zip(cs, bd.Tag)]
+    outs = bd.fused_kv_proj_grouped(xt, specs, out_layout=layout)
+    for c, t, o in zip(cs, bd.Tag, outs):
+        got = o.cpu().numpy()
+        if layout == "head":
+            got = got.transpose(1, 0, 2).reshape(L, n * d_h)
+        np.testing.assert_array_equal(got, O.fused_kv_proj_ref(x, c, d_h, n, t.value,
+                                                                threads=O.max_threads()))
+
+
 def test_exact_grouped_launch_equals_separate(cuda):
     rng = O.Rng(11)
     x = torch.from_numpy(O.rand_gaussian(rng, 70, 48, np.float32)).to(cuda)
