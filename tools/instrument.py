@@ -86,9 +86,9 @@ for lead in ("0", "lead"):
         if (it < 8) TL[32 + it] = CK();''')
 rep('''    if (lane == 0) tma_store_wait_all<0>();''', '''    if (lane == 0) tma_store_wait_all<0>();
     if (leader) { TL[40] = CK(); TL[41] = GT(); TL[42] = t_end - t_begin; }''')
-rep('''        const bool reload_a = P.num_kb > A_SLOTS || key != prev_key;
+rep('''        const bool reload_a = P.num_kb > A_SLOTS || key != prev_key;  // the resident operand
         prev_key = key;
-        const int my_m0''', '''        const bool reload_a = P.num_kb > A_SLOTS || key != prev_key;
+        const int my_m0''', '''        const bool reload_a = P.num_kb > A_SLOTS || key != prev_key;  // the resident operand
         if (t == t_begin && lane == 0) TL[43] = CK() + (reload_a ? 0 : 1);
         prev_key = key;
         const int my_m0''')
