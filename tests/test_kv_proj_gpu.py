@@ -340,15 +340,17 @@ def test_head_major_tc_needs_d_h_multiple_of_64(cuda):
         bd.fused_kv_proj(x, c, 8, 2, out_layout="head")
 
 
-@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("dtype,L", [(torch.float16, 700), (torch.bfloat16, 700),
+                                     (torch.float32, 700), (torch.float32, 3000)])
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
-def test_fused_allgather_single_device_ranks(dtype, world, cuda):
+def test_fused_allgather_single_device_ranks(dtype, L, world, cuda):
     """The all-gather fused into the epilogue, every 'rank' on one device: after each
     rank's launch with its head shard, EVERY rank's gathered buffer holds the full
     head-major K'/V' — bit-identical to the unsharded head-major projection (the
-    multi-GPU version differs only in the buffers being peer memory)."""
+    multi-GPU version differs only in the buffers being peer memory).  FP32 at L = 3000
+    takes the exact kernel's 128 x 128 tiles for world <= 2, its 64 x 64 tiles beyond."""
     from paper_2510_01718_b200 import parallel as P
-    L, d, d_h, n = 700, 512, 128, 16
+    d, d_h, n = 512, 128, 16
     g = torch.Generator().manual_seed(world)
     x = torch.randn(L, d, generator=g).to(dtype).to(cuda)
     ck = (torch.randn(d - d_h, n * d_h, generator=g) / 8).to(dtype).to(cuda)
