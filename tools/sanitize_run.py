@@ -37,6 +37,13 @@ def main():
         x = torch.randn(70, 100, generator=g).to(dt).to(dev)
         c = torch.randn(76, 72, generator=g).to(dt).to(dev)
         check(bd.fused_kv_proj(x, c, 24, 3, bd.Tag.LAST), ref(x, c, 24, 3, bd.Tag.LAST), tol)
+        # the 64 x 64 (L = 600) and 128 x 128 (L = 2400: >= 2 tiles per SM) tile kernels,
+        # ragged edges (K = 125, N = 2040)
+        for L in (600, 2400):
+            x = torch.randn(L, 133, generator=g).to(dt).to(dev)
+            c = torch.randn(125, 2040, generator=g).to(dt).to(dev)
+            check(bd.fused_kv_proj(x, c, 8, 255, bd.Tag.FIRST), ref(x, c, 8, 255, bd.Tag.FIRST),
+                  tol)
     for dt in (torch.float16, torch.bfloat16):
         tol = 2e-3 if dt == torch.float16 else 1.6e-2
         # persistent pair kernel, contiguous schedule, 2 problems, check on
