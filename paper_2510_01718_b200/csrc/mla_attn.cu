@@ -15,7 +15,8 @@
 //     applied to its pe columns in place).
 // so S = Q K^T is two accumulating groups of MMAs (K = 128 from K'_nope, K = 64 from k_pe).
 //
-// One persistent CTA per SM; work items (head, 128-query tile) in longest-first order.
+// One persistent CTA per SM; work items (head, 128-query tile) in L2-sized head groups,
+// each group longest-first (item_of).
 // Warp roles (192 threads):
 //   warp 0     TMA producer: Q tile (3 x 16 KB), per KV tile K'_nope + k_pe (48 KB) and
 //              V' (32 KB) through 2-stage rings.
@@ -38,6 +39,7 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <mutex>
@@ -74,6 +76,7 @@ struct AttnParams {
   void* out;             // O (t, h, c) at out + t * ldo_tok + h * ldo_head + c
   int64_t ldo_tok, ldo_head;
   int32_t L, H, n_qt, causal, total_items;
+  int32_t hgroup;        // heads per scheduling group (K/V of a group stays in L2)
   float scale_log2;      // softmax scale * log2(e)
 };
 
@@ -88,10 +91,17 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// item w -> (head, query tile), longest (latest) query tiles first
+// item w -> (head, query tile): heads in groups of hgroup, each group's items longest
+// (latest) query tile first.  The CTAs in flight then work on one or two groups, whose
+// K'/V' tiles (re-read by every later query tile of the same head) stay L2-resident; with
+// every head in flight at once the live K/V set exceeds L2 and is re-read from HBM.
 __device__ __forceinline__ void item_of(const AttnParams& p, int w, int& h, int& qi) {
-  qi = p.n_qt - 1 - w / p.H;
-  h = w % p.H;
+  const int per = p.hgroup * p.n_qt;
+  const int grp = w / per, r = w - grp * per;
+  const int rest = p.H - grp * p.hgroup;
+  const int gh = rest < p.hgroup ? rest : p.hgroup;
+  qi = p.n_qt - 1 - r / gh;
+  h = grp * p.hgroup + r % gh;
 }
 
 template <bool kBF16>
@@ -455,6 +465,18 @@ int launch_mla_attention(const MlaAttnArgs& a, cudaStream_t stream) {
   prm.n_qt = static_cast<int32_t>((a.L + BQ - 1) / BQ);
   prm.causal = a.causal ? 1 : 0;
   prm.total_items = prm.n_qt * prm.H;
+  {
+    // heads per group: the group's K'_nope + V' (2 x L x 128 x 2 bytes per head) within
+    // ~48 MB of the 126 MB L2; BD_ATTN_HGROUP overrides (A/B)
+    static const int env = [] {
+      const char* e = getenv("BD_ATTN_HGROUP");
+      return e != nullptr ? atoi(e) : 0;
+    }();
+    const int64_t per_head = a.L * (DN + DV) * 2;
+    int64_t g = (48ll << 20) / (per_head > 0 ? per_head : 1);
+    if (env > 0) g = env;
+    prm.hgroup = static_cast<int32_t>(g < 1 ? 1 : (g > prm.H ? prm.H : g));
+  }
   prm.scale_log2 = a.scale * 1.4426950408889634f;
   using KernFn = void (*)(AttnParams);
   const KernFn kern = bf16 ? mla_attn_kernel<true> : mla_attn_kernel<false>;
