@@ -91,6 +91,13 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// The k-th item of CTA b (of G): rounds of G items, alternate rounds in reverse CTA order
+// (items are sorted longest first, so a CTA's long and short items pair up).
+__device__ __forceinline__ int zz_item(int k, int G) {
+  const int b = static_cast<int>(blockIdx.x);
+  return k * G + ((k & 1) ? G - 1 - b : b);
+}
+
 // item w -> (head, query tile): heads in groups of hgroup, each group's items longest
 // (latest) query tile first.  The CTAs in flight then work on one or two groups, whose
 // K'/V' tiles (re-read by every later query tile of the same head) stay L2-resident; with
@@ -169,7 +176,7 @@ __global__ void __launch_bounds__(THREADS, 1) mla_attn_kernel(const __grid_const
     const uint64_t pol_q = policy_evict_first();
     const uint64_t pol_kv = policy_evict_last();  // K/V tiles are re-read by later queries
     uint32_t kv_it = 0, item_it = 0;
-    for (int w = static_cast<int>(blockIdx.x); w < prm.total_items; w += G, ++item_it) {
+    for (int zk = 0, w = zz_item(0, G); w < prm.total_items; w = zz_item(++zk, G), ++item_it) {
       int h, qi;
       item_of(prm, w, h, qi);
       const int n_kv = prm.causal ? qi + 1 : nkt_all;
@@ -229,7 +236,7 @@ __global__ void __launch_bounds__(THREADS, 1) mla_attn_kernel(const __grid_const
       ++kv_it_s;
       ++s_it;
     };
-    for (int w = static_cast<int>(blockIdx.x); w < prm.total_items; w += G, ++item_it) {
+    for (int zk = 0, w = zz_item(0, G); w < prm.total_items; w = zz_item(++zk, G), ++item_it) {
       int h, qi;
       item_of(prm, w, h, qi);
       const int n_kv = prm.causal ? qi + 1 : nkt_all;
@@ -273,7 +280,7 @@ __global__ void __launch_bounds__(THREADS, 1) mla_attn_kernel(const __grid_const
     const uint32_t lane_base = (quad * 32u) << 16;
     uint32_t s_it = 0, pv_it = 0;
     const float c2 = prm.scale_log2;
-    for (int w = static_cast<int>(blockIdx.x); w < prm.total_items; w += G) {
+    for (int zk = 0, w = zz_item(0, G); w < prm.total_items; w = zz_item(++zk, G)) {
       int h, qi;
       item_of(prm, w, h, qi);
       const int n_kv = prm.causal ? qi + 1 : nkt_all;
