@@ -6,7 +6,12 @@
 // issuing one piece multicast to all C: every SM still receives the same bytes, L2 serves
 // 1/C of them.  Same delivered bytes for C = 1, 2, 4 -> if the time drops with C, the L2
 // side (not the SM ports) is the shared limit and multicasting B across pairs would pay.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/mb tools/mcast_bw.cu
+// Loads are 1-D bulk copies (tensor = 0) or, like the projection's B stream, 2-D tensor-map
+// TMA boxes of 128 rows x 128 B with the 128-byte swizzle (tensor = 1; a cluster of C
+// splits each box into C sub-boxes of 128 / C rows, each multicast to all C CTAs).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/mb tools/mcast_bw.cu -lcuda
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <vector>
@@ -19,7 +24,7 @@ constexpr int LAG = 8;     // rounds in flight
 
 __global__ void __launch_bounds__(128, 1)
     k_mcast(uint8_t* __restrict__ dst, size_t W, const uint8_t* __restrict__ src, size_t S,
-            int do_store, float ratio, int C) {
+            int do_store, float ratio, int C, const __grid_constant__ CUtensorMap map, int tensor) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[NSLOT], freeb[NSLOT];
   const uint32_t rank = C > 1 ? cluster_ctarank() : 0;
@@ -62,7 +67,24 @@ __global__ void __launch_bounds__(128, 1)
         if (j >= NSLOT) mbar_wait(&freeb[s], ((j / NSLOT) - 1) & 1);
         mbar_arrive_expect_tx(&full[s], CH);
         const size_t off = (static_cast<size_t>(j) * CH) % sper + rank * piece;
-        if (C == 1)
+        if (tensor) {
+          // 128-row box split into C sub-boxes; row coordinate of this CTA's piece
+          const int row = static_cast<int>((sper * (blockIdx.x / C) + off) / 128);
+          if (C == 1)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(ring + s * CH)),
+                "l"(reinterpret_cast<uint64_t>(&map)), "r"(0), "r"(row), "r"(smem_u32(&full[s]))
+                : "memory");
+          else
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
+                    smem_u32(ring + s * CH + rank * piece)),
+                "l"(reinterpret_cast<uint64_t>(&map)), "r"(0), "r"(row), "r"(smem_u32(&full[s])),
+                "h"(mask)
+                : "memory");
+        } else if (C == 1)
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                   smem_u32(ring + s * CH)),
@@ -101,10 +123,25 @@ int main() {
   uint8_t* src;
   cudaMalloc(&src, S);
   cudaMemset(src, 1, S);
-  struct V { int store; float ratio; int C; };
-  for (V v : {V{1, 0.f, 1}, V{0, 1.5f, 1}, V{0, 1.5f, 2}, V{0, 1.5f, 4}, V{1, 1.0f, 1},
-              V{1, 1.0f, 2}, V{1, 1.5f, 1}, V{1, 1.5f, 2}, V{1, 1.5f, 4}, V{1, 2.0f, 1},
-              V{1, 2.0f, 2}}) {
+  // tensor maps over src as [S / 128 rows][64 x 16-bit], box {64, 128 / C}, 128-B swizzle
+  void* fp = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fp, 12000, cudaEnableDefault, &q);
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fp);
+  CUtensorMap maps[5];
+  for (int c : {1, 2, 4}) {
+    cuuint64_t dims[2] = {64, S / 128};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(128 / c)}, es[2] = {1, 1};
+    encode(&maps[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, src, dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  struct V { int store; float ratio; int C; int tensor; };
+  for (V v : {V{1, 0.f, 1, 0}, V{0, 1.5f, 1, 0}, V{0, 1.5f, 2, 0}, V{1, 1.5f, 1, 0},
+              V{1, 1.5f, 2, 0}, V{0, 1.5f, 1, 1}, V{0, 1.5f, 2, 1}, V{0, 1.5f, 4, 1},
+              V{1, 1.5f, 1, 1}, V{1, 1.5f, 2, 1}, V{1, 1.5f, 4, 1}, V{1, 2.0f, 1, 1},
+              V{1, 2.0f, 2, 1}}) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(148);
     cfg.blockDim = dim3(128);
@@ -123,7 +160,7 @@ int main() {
     cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal);
     for (int i = 0; i < inner; ++i)
       cudaLaunchKernelEx(&cfg, k_mcast, dst[i % R], W, (const uint8_t*)src, S, v.store, v.ratio,
-                         v.C);
+                         v.C, maps[v.C], v.tensor);
     cudaStreamEndCapture(s, &g);
     cudaGraphInstantiate(&ge, g, 0);
     cudaGraphLaunch(ge, s);
@@ -142,9 +179,9 @@ int main() {
       best = ms < best ? ms : best;
     }
     const double us = best * 1000 / inner;
-    printf("store %d load ratio %.1f cluster %d: %7.2f us -> stores %6.0f GB/s, loads delivered "
+    printf("%s store %d load ratio %.1f cluster %d: %7.2f us -> stores %6.0f GB/s, loads delivered "
            "%6.0f GB/s (L2 reads %6.0f GB/s)  %s\n",
-           v.store, v.ratio, v.C, us, v.store ? W / us / 1e3 : 0.0, W * v.ratio / us / 1e3,
+           v.tensor ? "tensor" : "bulk  ", v.store, v.ratio, v.C, us, v.store ? W / us / 1e3 : 0.0, W * v.ratio / us / 1e3,
            W * v.ratio / v.C / us / 1e3, cudaGetErrorString(cudaGetLastError()));
     cudaGraphExecDestroy(ge);
     cudaGraphDestroy(g);
