@@ -727,10 +727,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 
 // ---------------------------------------------------------------------------------
-// Small-L ("decode") kernel: L <= 128 tokens, K <= 384.  The persistent pair kernel
-// spends a full 256-row tile, its prologue and a 256-column epilogue per output block —
-// ~8 us whatever L is.  Here each CTA owns one BNS-column block of one problem for all
-// (<= 128) rows: its whole A (x rows, L x K) and B (K x BNS) slices are loaded at once
+// Small-L ("decode") kernel: L <= 512 tokens (while the CTAs fit one wave), K <= 384.
+// The persistent pair kernel spends a full 256-row tile, its prologue and a 256-column
+// epilogue per output block — ~8 us whatever L is.  Here each CTA owns one BNS-column
+// block of one problem for one 128-row block (all rows when L <= 128): its whole A (x
+// rows, <= 128 x K) and B (K x BNS) slices are loaded at once
 // (one barrier per 64-deep k-block so the MMAs start on the first), one M=128 x N=BNS
 // accumulator in TMEM (cta_group::1), and four epilogue warps add the repeated slice
 // (global loads, L2-resident), round and store straight to global memory.  The work is
@@ -1134,18 +1135,25 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     cols += probs[i].N;
     max_l = probs[i].L > max_l ? probs[i].L : max_l;
   }
-  // L <= 128: single CTAs (M = 128); 128 < L <= 256: CTA pairs (M = 256, each CTA its 128
-  // rows of A and half of the column block's B)
-  const int cgs = max_l > BM ? 2 : 1;
+  // One CTA (M = 128) per (128-row block, column block).  BD_SMALL_PAIRS=1 (A/B) runs
+  // L > 128 on CTA pairs instead (M = 256, each CTA its 128 rows of A and half of the
+  // column block's B): half the CTAs, and measured slower — cfg2 K'+V' L = 256 / 384 /
+  // 512: 4.69 / 5.95 / 5.99 us on pairs, 4.32 / 4.75 / 5.11 on single CTAs
+  // (tools/small_single_ab.sh)
+  static const bool pairs = [] {
+    const char* e = getenv("BD_SMALL_PAIRS");
+    return e != nullptr && atoi(e) == 1;
+  }();
+  const int cgs = max_l > BM && pairs ? 2 : 1;
   const int nrb = static_cast<int>((max_l + BM * cgs - 1) / (BM * cgs));  // row blocks
-  const int a_rows = cgs == 2 ? BM : static_cast<int>((max_l + 7) / 8 * 8);
+  const int a_rows = cgs == 2 || max_l > BM ? BM : static_cast<int>((max_l + 7) / 8 * 8);
   const int a_kb_bytes = a_rows * BK * 2;
   int bns;
   if (cgs == 1) {
     // Column block: 64 when the CTAs that gives fit in one wave at two CTAs per SM, else
     // 128 (C streams through as many SMs as possible in a single wave)
     const int per_sm64 = small_smem_bytes(64, a_kb_bytes, false) * 2 <= 232448 ? 2 : 1;
-    bns = (cols + 63) / 64 <= static_cast<int64_t>(per_sm64) * sm_count() ? 64 : 128;
+    bns = (cols + 63) / 64 * nrb <= static_cast<int64_t>(per_sm64) * sm_count() ? 64 : 128;
     static const int bns_env = [] {  // BD_SMALL_BNS=64|128: force the column block (A/B)
       const char* e = getenv("BD_SMALL_BNS");
       return e != nullptr ? atoi(e) : 0;

@@ -62,7 +62,7 @@ def main():
         a, b = bd.fused_kv_proj_grouped(x2, [(c8, 8, 8, bd.Tag.FIRST), (c128, 128, 4, bd.Tag.LAST)])
         check(a, ref(x2, c8, 8, 8, bd.Tag.FIRST), tol)
         check(b, ref(x2, c128, 128, 4, bd.Tag.LAST), tol)
-        # small-L kernel: single CTA (L <= 128) and pair (128 < L <= 256)
+        # small-L kernel: one row block (L <= 128) and two 128-row blocks (L = 200)
         for L in (40, 200):
             k, v = bd.fused_kv_proj_grouped(x[:L].contiguous(), [(ck, 128, 8, bd.Tag.FIRST),
                                                                  (cv, 128, 8, bd.Tag.LAST)])

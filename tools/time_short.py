@@ -15,7 +15,7 @@ dev = torch.device("cuda:0")
 g = torch.Generator(device=dev).manual_seed(3)
 h = torch.float16
 cases = [("paper", L, 128, 1) for L in (64, 128, 256, 512, 1024, 4096)] + \
-        [("cfg2", L, 16, 2) for L in (256, 1024, 8192)]
+        [("cfg2", L, 16, 2) for L in (64, 128, 160, 256, 384, 512, 1024, 8192)]
 out = []
 for name, L, n, probs in cases:
     d, d_h = 512, 128
