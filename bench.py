@@ -732,12 +732,15 @@ def run_configs(torch, dev, peak_tf, peak_hbm):
                 for s in sets]
             est = 4 + 2 * L * d * N * nprob / 1.2e9
             inner = inner_for(est, R)
-            us = time_ring_us(calls, inner)
+            # decode-sized points last a few µs: more replays for a stable median
+            reps = 11 if est < 20 else 5
+            us = time_ring_us(calls, inner, reps=reps)
             dsets = [(s[0], rnd((d, nprob * N), dtype, 1 / 8),
                       torch.empty(L, nprob * N, device=dev, dtype=dtype)) for s in sets]
             del calls
             sets = None
-            dus = time_ring_us([lambda s=s: torch.matmul(s[0], s[1], out=s[2]) for s in dsets], inner)
+            dus = time_ring_us([lambda s=s: torch.matmul(s[0], s[1], out=s[2]) for s in dsets], inner,
+                               reps=reps)
             del dsets
             flops = 2 * L * K * N * nprob
             nbytes = 2 * (L * d + nprob * (K * N + L * N))
