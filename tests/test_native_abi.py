@@ -140,3 +140,19 @@ def test_rmsnorm_and_allgather_entries_reject_bad_arguments(lib):
     assert lib.bd_kv_proj_grouped_allgather(p, 1, N.BD_F16, 0, 2, 2, bufs, None, None) == N.BD_ERR_ARG
     assert lib.bd_kv_proj_grouped_allgather(p, 1, N.BD_F16, 0, 2, 0, None, None, None) == N.BD_ERR_ARG
     assert lib.bd_launch_count() == before
+
+
+@pytest.mark.parametrize("L,chunks", [(0, 4), (1, 4), (255, 4), (300, 4), (8192, 4), (8192, 1),
+                                      (8192, 3), (65536, 8), (1000, 100)])
+def test_host_pipeline_row_blocks_partition_the_tokens(L, chunks):
+    """The host pipeline's row blocks tile [0, L) exactly, in order, each a whole number of
+    256-row CTA-pair tiles except the last (host logic of fused_kv_proj_grouped_host)."""
+    from paper_2510_01718_b200.kv_proj import _chunk_bounds
+    b = _chunk_bounds(L, chunks)
+    if L == 0:
+        assert b == []
+        return
+    assert b[0][0] == 0 and b[-1][1] == L
+    assert all(x[1] == y[0] for x, y in zip(b, b[1:]))
+    assert all((r1 - r0) % 256 == 0 for r0, r1 in b[:-1])
+    assert len(b) <= max(1, chunks)
