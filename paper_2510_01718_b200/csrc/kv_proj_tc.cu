@@ -741,7 +741,7 @@ constexpr int SM_THREADS = 64 + 128;  // producer, MMA, 4 epilogue warps
 constexpr int SM_MAX_KB = 6;          // K <= 384
 constexpr uint32_t SM_STG = 4 * 2 * STG_BYTES;  // pair variant: 2 staging boxes per epilogue warp
 inline size_t small_smem_bytes(int bns_per_cta, int a_kb_bytes, bool tma_store) {
-  return 1024 + SM_MAX_KB * (a_kb_bytes + (bns_per_cta / 64) * B_PANEL) +
+  return 1024 + SM_MAX_KB * (a_kb_bytes + bns_per_cta * BKB * 2) +
          (tma_store ? SM_STG : 0) + 128;
 }
 
@@ -750,8 +750,13 @@ inline size_t small_smem_bytes(int bns_per_cta, int a_kb_bytes, bool tma_store) 
 template <bool kBF16, bool kCheck, int BNS, int CGS>
 __global__ void __launch_bounds__(SM_THREADS, 1)
     kv_proj_small_kernel(const __grid_constant__ TcParams prm) {
-  constexpr int PANELS = BNS / CGS / 64;
-  constexpr uint32_t BS_BYTES = PANELS * B_PANEL;  // one k-block of this CTA's B
+  // B panels: 64 columns with the 128-byte swizzle, or one 32-column panel with the
+  // 64-byte swizzle (BNS = 32: twice the CTAs on decode-sized, narrow launches)
+  constexpr int PW = BNS / CGS < 64 ? BNS / CGS : 64;
+  constexpr int PANELS = BNS / CGS / PW;
+  constexpr uint32_t PANEL_BYTES = PW * BKB * 2;
+  constexpr uint32_t BS_BYTES = PANELS * PANEL_BYTES;  // one k-block of this CTA's B
+  constexpr uint32_t B_LAYOUT = PW == 64 ? 2u : 4u;     // SWIZZLE_128B / SWIZZLE_64B
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -800,7 +805,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1)
       for (int q = 0; q < PANELS; ++q)
         asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
                          reinterpret_cast<uint64_t>(&P.map_b)),
-                     "r"(my_n0 + 64 * q), "r"(kb * BK)
+                     "r"(my_n0 + PW * q), "r"(kb * BK)
                      : "memory");
   }
   if (warp == 1) {
@@ -828,13 +833,13 @@ __global__ void __launch_bounds__(SM_THREADS, 1)
           const uint32_t bar = mapa_shared(smem_u32(&full[kb]), 0);
           tma_load_2d_pair(sA + kb * a_kb, &P.map_a, kb * BK, m0, bar, pol);
           for (int q = 0; q < PANELS; ++q)
-            tma_load_2d_pair(sB + kb * BS_BYTES + q * B_PANEL, &P.map_b, my_n0 + 64 * q,
+            tma_load_2d_pair(sB + kb * BS_BYTES + q * PANEL_BYTES, &P.map_b, my_n0 + PW * q,
                              kb * BK, bar, pol);
         } else {
           mbar_arrive_expect_tx(&full[kb], a_kb + BS_BYTES);
           tma_load_2d(sA + kb * a_kb, &P.map_a, kb * BK, m0, &full[kb], pol);
           for (int q = 0; q < PANELS; ++q)
-            tma_load_2d(sB + kb * BS_BYTES + q * B_PANEL, &P.map_b, my_n0 + 64 * q, kb * BK,
+            tma_load_2d(sB + kb * BS_BYTES + q * PANEL_BYTES, &P.map_b, my_n0 + PW * q, kb * BK,
                         &full[kb], pol);
         }
       }
@@ -854,7 +859,8 @@ __global__ void __launch_bounds__(SM_THREADS, 1)
 #pragma unroll
           for (int ks = 0; ks < BK / UK; ++ks) {
             const uint64_t ad = make_smem_desc(a0 + ks * (UK * 2), 16, 1024);
-            const uint64_t bdsc = make_smem_desc(b0 + ks * (UK * 128), B_PANEL, 1024);
+            const uint64_t bdsc =
+                make_smem_desc_sw(b0 + ks * (UK * PW * 2), PANEL_BYTES, 8 * PW * 2, B_LAYOUT);
             if constexpr (CGS == 2)
               tc_mma_f16_pair(tmem_base, ad, bdsc, idesc, (kb | ks) != 0 ? 1u : 0u);
             else
@@ -1154,11 +1160,14 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     // 128 (C streams through as many SMs as possible in a single wave)
     const int per_sm64 = small_smem_bytes(64, a_kb_bytes, false) * 2 <= 232448 ? 2 : 1;
     bns = (cols + 63) / 64 * nrb <= static_cast<int64_t>(per_sm64) * sm_count() ? 64 : 128;
-    static const int bns_env = [] {  // BD_SMALL_BNS=64|128: force the column block (A/B)
+    // 32 when even 32-column blocks give every CTA its own SM: the shortest MMA chain
+    // and B slice per CTA, the most SMs pulling C in
+    if ((cols + 31) / 32 * nrb <= static_cast<int64_t>(sm_count())) bns = 32;
+    static const int bns_env = [] {  // BD_SMALL_BNS=32|64|128: force the column block (A/B)
       const char* e = getenv("BD_SMALL_BNS");
       return e != nullptr ? atoi(e) : 0;
     }();
-    if (bns_env == 64 || bns_env == 128) bns = bns_env;
+    if (bns_env == 32 || bns_env == 64 || bns_env == 128) bns = bns_env;
   } else {
     // pairs: one CTA per SM (A is 96 KiB); 256-column blocks once they fill a wave
     bns = (cols + 127) / 128 * nrb <= static_cast<int64_t>(sm_count() / 2) ? 128 : 256;
@@ -1177,7 +1186,8 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     const bool has_rep = q.rep_base >= 0;
     const auto* xb = static_cast<const uint16_t*>(q.x) + q.mul_base;
     if (!encode_2d(&P.map_a, xb, bf16, q.K, q.L, q.ldx, BK, a_rows, &err) ||
-        !encode_2d(&P.map_b, q.c, bf16, q.N, q.K, q.ldc, 64, BK, &err) ||
+        !encode_2d(&P.map_b, q.c, bf16, q.N, q.K, q.ldc, bns / cgs < 64 ? bns / cgs : 64, BK,
+                   &err, bns / cgs < 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B) ||
         (tma_st &&
          !(q.out_layout == BD_OUT_HEAD_MAJOR
                ? encode_3d(&P.map_out, q.out, bf16, q.d_h, q.L, q.N / q.d_h, q.ldo,
@@ -1206,23 +1216,27 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
   prm.total_tiles = total;
   if (total == 0) return BD_OK;
   using KernFn = void (*)(TcParams);
-  // [bf16][check][0: 1 CTA x 64, 1: 1 CTA x 128, 2: pair x 128, 3: pair x 256]
-  static const KernFn kerns[2][2][4] = {
+  // [bf16][check][0: 1 CTA x 64, 1: 1 CTA x 128, 2: pair x 128, 3: pair x 256, 4: 1 CTA x 32]
+  static const KernFn kerns[2][2][5] = {
       {{kv_proj_small_kernel<false, false, 64, 1>, kv_proj_small_kernel<false, false, 128, 1>,
-        kv_proj_small_kernel<false, false, 128, 2>, kv_proj_small_kernel<false, false, 256, 2>},
+        kv_proj_small_kernel<false, false, 128, 2>, kv_proj_small_kernel<false, false, 256, 2>,
+        kv_proj_small_kernel<false, false, 32, 1>},
        {kv_proj_small_kernel<false, true, 64, 1>, kv_proj_small_kernel<false, true, 128, 1>,
-        kv_proj_small_kernel<false, true, 128, 2>, kv_proj_small_kernel<false, true, 256, 2>}},
+        kv_proj_small_kernel<false, true, 128, 2>, kv_proj_small_kernel<false, true, 256, 2>,
+        kv_proj_small_kernel<false, true, 32, 1>}},
       {{kv_proj_small_kernel<true, false, 64, 1>, kv_proj_small_kernel<true, false, 128, 1>,
-        kv_proj_small_kernel<true, false, 128, 2>, kv_proj_small_kernel<true, false, 256, 2>},
+        kv_proj_small_kernel<true, false, 128, 2>, kv_proj_small_kernel<true, false, 256, 2>,
+        kv_proj_small_kernel<true, false, 32, 1>},
        {kv_proj_small_kernel<true, true, 64, 1>, kv_proj_small_kernel<true, true, 128, 1>,
-        kv_proj_small_kernel<true, true, 128, 2>, kv_proj_small_kernel<true, true, 256, 2>}}};
+        kv_proj_small_kernel<true, true, 128, 2>, kv_proj_small_kernel<true, true, 256, 2>,
+        kv_proj_small_kernel<true, true, 32, 1>}}};
   const int vb = bf16 ? 1 : 0, vc = flag != nullptr ? 1 : 0;
-  const int vn = cgs == 1 ? (bns == 128 ? 1 : 0) : (bns == 256 ? 3 : 2);
+  const int vn = cgs == 1 ? (bns == 128 ? 1 : bns == 32 ? 4 : 0) : (bns == 256 ? 3 : 2);
   const KernFn kern = kerns[vb][vc][vn];
   const size_t smem = small_smem_bytes(bns / cgs, a_kb_bytes, tma_st);
   // the attribute belongs to the function in the CURRENT device's context: set it once
   // per device ordinal
-  static std::atomic<bool> attr_done[kMaxDevices][2][2][4] = {};
+  static std::atomic<bool> attr_done[kMaxDevices][2][2][5] = {};
   static std::mutex attr_mu;
   const int dv = device_slot();
   if (!attr_done[dv][vb][vc][vn].load(std::memory_order_acquire)) {

@@ -358,15 +358,20 @@ __device__ __forceinline__ void tmem_ld_wait() {
 //   [32,46) stride-dimension byte offset >> 4   [46,48) version = 1 (sm_100)
 //   [49,52) base offset = 0           [52]    LBO mode = 0
 //   [61,64) layout: 0 none, 2 SWIZZLE_128B, 4 SWIZZLE_64B, 6 SWIZZLE_32B
-__device__ __forceinline__ uint64_t make_smem_desc(uint32_t saddr, uint32_t lbo_bytes,
-                                                   uint32_t sbo_bytes) {
+// layout: 2 = SWIZZLE_128B, 4 = SWIZZLE_64B (sm100 encoding, bits [61, 64))
+__device__ __forceinline__ uint64_t make_smem_desc_sw(uint32_t saddr, uint32_t lbo_bytes,
+                                                      uint32_t sbo_bytes, uint32_t layout) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
   d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
   d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
   d |= static_cast<uint64_t>(1) << 46;  // version
-  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  d |= static_cast<uint64_t>(layout) << 61;
   return d;
+}
+__device__ __forceinline__ uint64_t make_smem_desc(uint32_t saddr, uint32_t lbo_bytes,
+                                                   uint32_t sbo_bytes) {
+  return make_smem_desc_sw(saddr, lbo_bytes, sbo_bytes, 2u);  // SWIZZLE_128B
 }
 
 // Instruction descriptor for kind::f16 with F32 accumulation.
