@@ -15,7 +15,10 @@ dev = torch.device("cuda:0")
 g = torch.Generator(device=dev).manual_seed(3)
 h = torch.float16
 cases = [("paper", L, 128, 1) for L in (64, 128, 256, 512, 1024, 4096)] + \
-        [("cfg2", L, 16, 2) for L in (64, 128, 160, 256, 384, 512, 1024, 8192)]
+        [("cfg2", L, 16, 2) for L in (64, 128, 160, 256, 384, 512, 640, 768, 1024, 8192)]
+if os.environ.get("TIME_SHORT_CASES"):  # e.g. "cfg2:640,cfg2:1024"
+    cases = [(c.split(":")[0], int(c.split(":")[1]), 128 if c.startswith("paper") else 16,
+              1 if c.startswith("paper") else 2) for c in os.environ["TIME_SHORT_CASES"].split(",")]
 out = []
 for name, L, n, probs in cases:
     d, d_h = 512, 128
