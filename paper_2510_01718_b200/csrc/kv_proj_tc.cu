@@ -229,8 +229,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < A_SLOTS; ++s) {
       mbar_init(&a_full[s], 1);   // armed by the leader's producer with the pair's bytes
-      // one multicast tcgen05.commit (+ kNorm: this CTA's epilogue, done reading the slot)
-      mbar_init(&a_empty[s], kNorm ? 2 : 1);
+      // one multicast tcgen05.commit (+ kNorm: each of this CTA's four epilogue lane
+      // quadrants, done reading the slot)
+      mbar_init(&a_empty[s], kNorm ? 1 + 4 : 1);
     }
     for (int s = 0; s < BST; ++s) {
       mbar_init(&b_full[s], 1);
@@ -561,15 +562,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               }
             }
           }
+          // the two warps of this lane quadrant meet (named barrier 4 + quad, 64 threads):
+          // the other quadrants run on, their warps not held at a CTA-wide barrier
           norm_part[half * BM + row_t] = (ssv[0] + ssv[1]) + (ssv[2] + ssv[3]);
-          named_bar_sync(3, 32 * EPI_WARPS);
+          named_bar_sync(4 + quad, 64);
           const float tot = norm_part[row_t] + norm_part[BM + row_t];
           // rows past L are TMA zero-fill: with eps == 0 their rsqrt would be inf and
           // 0 * inf a NaN that trips the non-finite check — they are never stored, use 0
           rnorm = my_m0 + row_t < P.L ? rsqrtf(tot / static_cast<float>(P.norm_d) + P.norm_eps)
                                       : 0.f;
-          named_bar_sync(3, 32 * EPI_WARPS);  // everyone read the A slots and the partials
-          if (leader)
+          named_bar_sync(4 + quad, 64);  // this quadrant read its A rows and the partials
+          if (half == 0 && lane == 0)
             for (int kb = 0; kb < nkb; ++kb)
               mbar_arrive(&a_empty[(ep_a_base + static_cast<uint32_t>(kb)) % A_SLOTS]);
           const int dm = P.d_h - 1;
