@@ -753,13 +753,16 @@ inline size_t small_smem_bytes(int bns_per_cta, int a_kb_bytes, bool tma_store) 
 template <bool kBF16, bool kCheck, int BNS, int CGS>
 __global__ void __launch_bounds__(SM_THREADS, 1)
     kv_proj_small_kernel(const __grid_constant__ TcParams prm) {
-  // B panels: 64 columns with the 128-byte swizzle, or one 32-column panel with the
-  // 64-byte swizzle (BNS = 32: twice the CTAs on decode-sized, narrow launches)
-  constexpr int PW = BNS / CGS < 64 ? BNS / CGS : 64;
+  // B panels: 64 columns with the 128-byte swizzle, or 32-column panels with the 64-byte
+  // swizzle for column blocks that are not a multiple of 64 (32, 96, 160: one wave of
+  // CTAs on decode-sized, narrow launches)
+  constexpr int PW = (BNS / CGS) % 64 == 0 ? 64 : 32;
   constexpr int PANELS = BNS / CGS / PW;
   constexpr uint32_t PANEL_BYTES = PW * BKB * 2;
   constexpr uint32_t BS_BYTES = PANELS * PANEL_BYTES;  // one k-block of this CTA's B
   constexpr uint32_t B_LAYOUT = PW == 64 ? 2u : 4u;     // SWIZZLE_128B / SWIZZLE_64B
+  // TMEM allocations are powers of two >= 32 columns
+  constexpr uint32_t TCOLS = BNS <= 32 ? 32 : BNS <= 64 ? 64 : BNS <= 128 ? 128 : 256;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -812,7 +815,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1)
                      : "memory");
   }
   if (warp == 1) {
-    tmem_alloc<CGS>(tmem_slot, BNS);
+    tmem_alloc<CGS>(tmem_slot, TCOLS);
     tmem_relinquish<CGS>();
   }
   tc_fence_before();
@@ -1002,7 +1005,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1)
     __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<CGS>(tmem_base, BNS);
+    tmem_dealloc<CGS>(tmem_base, TCOLS);
   }
 }
 
@@ -1136,6 +1139,22 @@ int launch_params(const tc::TcParams& prm, int total, bool bf16, bool check,
 
 }  // namespace
 
+// Column block of the single-CTA small kernel for `cols` columns in `nrb` 128-row blocks:
+// the narrowest of 32 / 64 / 128 / 160 whose CTAs fit one wave (64 may run two CTAs per
+// SM when its shared memory allows), or 0 when none does.  (96 is instantiated for A/B —
+// BD_SMALL_BNS=96 — but at three row blocks it measured slower than 128: cfg2 L = 384
+// 4.95 vs 4.79 us; 160 at five row blocks beats the persistent kernel: L = 640 6.82 vs
+// 7.65 us, tools/small_bns_wave_ab.sh.)
+int small_bns_one_wave(int64_t cols, int64_t nrb, int a_kb_bytes) {
+  const int64_t sms = sm_count();
+  const int per_sm64 = tc::small_smem_bytes(64, a_kb_bytes, false) * 2 <= 232448 ? 2 : 1;
+  for (int b : {32, 64, 128, 160}) {
+    if (tc::small_smem_bytes(b, a_kb_bytes, b == 128) > 232448) continue;
+    if ((cols + b - 1) / b * nrb <= (b == 64 ? per_sm64 : 1) * sms) return b;
+  }
+  return 0;
+}
+
 // Small-L launch: one CTA per BNS-column block of each problem (no clusters).
 int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStream_t stream) {
   using namespace tc;
@@ -1159,18 +1178,17 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
   const int a_kb_bytes = a_rows * BK * 2;
   int bns;
   if (cgs == 1) {
-    // Column block: 64 when the CTAs that gives fit in one wave at two CTAs per SM, else
-    // 128 (C streams through as many SMs as possible in a single wave)
-    const int per_sm64 = small_smem_bytes(64, a_kb_bytes, false) * 2 <= 232448 ? 2 : 1;
-    bns = (cols + 63) / 64 * nrb <= static_cast<int64_t>(per_sm64) * sm_count() ? 64 : 128;
-    // 32 when even 32-column blocks give every CTA its own SM: the shortest MMA chain
-    // and B slice per CTA, the most SMs pulling C in
-    if ((cols + 31) / 32 * nrb <= static_cast<int64_t>(sm_count())) bns = 32;
-    static const int bns_env = [] {  // BD_SMALL_BNS=32|64|128: force the column block (A/B)
+    // Column block: the narrowest whose CTAs fit one wave (the shortest MMA chain and B
+    // slice per CTA, the most SMs pulling C in); 128 when none does (L <= 128 on wide
+    // problems: several waves)
+    bns = small_bns_one_wave(cols, nrb, a_kb_bytes);
+    if (bns == 0) bns = 128;
+    static const int bns_env = [] {  // BD_SMALL_BNS=32|64|96|128|160: force it (A/B)
       const char* e = getenv("BD_SMALL_BNS");
       return e != nullptr ? atoi(e) : 0;
     }();
-    if (bns_env == 32 || bns_env == 64 || bns_env == 128) bns = bns_env;
+    if (bns_env == 32 || bns_env == 64 || bns_env == 96 || bns_env == 128 || bns_env == 160)
+      bns = bns_env;
   } else {
     // pairs: one CTA per SM (A is 96 KiB); 256-column blocks once they fill a wave
     bns = (cols + 127) / 128 * nrb <= static_cast<int64_t>(sm_count() / 2) ? 128 : 256;
@@ -1189,8 +1207,9 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
     const bool has_rep = q.rep_base >= 0;
     const auto* xb = static_cast<const uint16_t*>(q.x) + q.mul_base;
     if (!encode_2d(&P.map_a, xb, bf16, q.K, q.L, q.ldx, BK, a_rows, &err) ||
-        !encode_2d(&P.map_b, q.c, bf16, q.N, q.K, q.ldc, bns / cgs < 64 ? bns / cgs : 64, BK,
-                   &err, bns / cgs < 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !encode_2d(&P.map_b, q.c, bf16, q.N, q.K, q.ldc, (bns / cgs) % 64 == 0 ? 64 : 32, BK,
+                   &err,
+                   (bns / cgs) % 64 == 0 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B) ||
         (tma_st &&
          !(q.out_layout == BD_OUT_HEAD_MAJOR
                ? encode_3d(&P.map_out, q.out, bf16, q.d_h, q.L, q.N / q.d_h, q.ldo,
@@ -1219,27 +1238,25 @@ int launch_small(const Problem* probs, int count, bool bf16, int* flag, cudaStre
   prm.total_tiles = total;
   if (total == 0) return BD_OK;
   using KernFn = void (*)(TcParams);
-  // [bf16][check][0: 1 CTA x 64, 1: 1 CTA x 128, 2: pair x 128, 3: pair x 256, 4: 1 CTA x 32]
-  static const KernFn kerns[2][2][5] = {
-      {{kv_proj_small_kernel<false, false, 64, 1>, kv_proj_small_kernel<false, false, 128, 1>,
-        kv_proj_small_kernel<false, false, 128, 2>, kv_proj_small_kernel<false, false, 256, 2>,
-        kv_proj_small_kernel<false, false, 32, 1>},
-       {kv_proj_small_kernel<false, true, 64, 1>, kv_proj_small_kernel<false, true, 128, 1>,
-        kv_proj_small_kernel<false, true, 128, 2>, kv_proj_small_kernel<false, true, 256, 2>,
-        kv_proj_small_kernel<false, true, 32, 1>}},
-      {{kv_proj_small_kernel<true, false, 64, 1>, kv_proj_small_kernel<true, false, 128, 1>,
-        kv_proj_small_kernel<true, false, 128, 2>, kv_proj_small_kernel<true, false, 256, 2>,
-        kv_proj_small_kernel<true, false, 32, 1>},
-       {kv_proj_small_kernel<true, true, 64, 1>, kv_proj_small_kernel<true, true, 128, 1>,
-        kv_proj_small_kernel<true, true, 128, 2>, kv_proj_small_kernel<true, true, 256, 2>,
-        kv_proj_small_kernel<true, true, 32, 1>}}};
+  // [bf16][check][0: 1 CTA x 64, 1: 1 CTA x 128, 2: pair x 128, 3: pair x 256,
+  //               4: 1 CTA x 32, 5: 1 CTA x 96, 6: 1 CTA x 160]
+#define BD_SMALL_ROW(B, C)                                                                   \
+  {kv_proj_small_kernel<B, C, 64, 1>, kv_proj_small_kernel<B, C, 128, 1>,                    \
+   kv_proj_small_kernel<B, C, 128, 2>, kv_proj_small_kernel<B, C, 256, 2>,                   \
+   kv_proj_small_kernel<B, C, 32, 1>, kv_proj_small_kernel<B, C, 96, 1>,                     \
+   kv_proj_small_kernel<B, C, 160, 1>}
+  static const KernFn kerns[2][2][7] = {
+      {BD_SMALL_ROW(false, false), BD_SMALL_ROW(false, true)},
+      {BD_SMALL_ROW(true, false), BD_SMALL_ROW(true, true)}};
+#undef BD_SMALL_ROW
   const int vb = bf16 ? 1 : 0, vc = flag != nullptr ? 1 : 0;
-  const int vn = cgs == 1 ? (bns == 128 ? 1 : bns == 32 ? 4 : 0) : (bns == 256 ? 3 : 2);
+  const int vn = cgs == 1 ? (bns == 128 ? 1 : bns == 32 ? 4 : bns == 96 ? 5 : bns == 160 ? 6 : 0)
+                          : (bns == 256 ? 3 : 2);
   const KernFn kern = kerns[vb][vc][vn];
   const size_t smem = small_smem_bytes(bns / cgs, a_kb_bytes, tma_st);
   // the attribute belongs to the function in the CURRENT device's context: set it once
   // per device ordinal
-  static std::atomic<bool> attr_done[kMaxDevices][2][2][5] = {};
+  static std::atomic<bool> attr_done[kMaxDevices][2][2][7] = {};
   static std::mutex attr_mu;
   const int dv = device_slot();
   if (!attr_done[dv][vb][vc][vn].load(std::memory_order_acquire)) {
@@ -1288,7 +1305,7 @@ bool small_eligible(const Problem* probs, int count) {
   if (off) return false;
   static const int max_l_env = [] {  // BD_SMALL_MAXL: development A/B of the L range
     const char* e = getenv("BD_SMALL_MAXL");
-    return e != nullptr ? atoi(e) : 4 * tc::BM;  // row blocks of pairs up to L = 512
+    return e != nullptr ? atoi(e) : 5 * tc::BM;  // up to five 128-row blocks
   }();
   static const bool wide = [] {  // BD_SMALL_WIDE=1: pairs also for wide problems
     const char* e = getenv("BD_SMALL_WIDE");
@@ -1302,11 +1319,11 @@ bool small_eligible(const Problem* probs, int count) {
     cols += probs[i].N;
     max_l = probs[i].L > max_l ? probs[i].L : max_l;
   }
-  // L > 128 (CTA pairs): only while 128-column blocks fill at most one wave of pairs
-  // per row block — wider problems run faster on the persistent kernel (measured: n =
-  // 128 heads, L = 256: 10.5 vs 8.1 us)
-  const int64_t nrb = (max_l + 2 * tc::BM - 1) / (2 * tc::BM);
-  if (!wide && max_l > tc::BM && nrb * cols > static_cast<int64_t>(sm_count() / 2) * 128)
+  // L > 128: only while the row blocks' CTAs fit one wave — wider or longer launches run
+  // faster on the persistent kernel (measured: n = 128 heads, L = 256: 10.3 vs 8.6 us;
+  // cfg2 L = 768: 9.2 vs 7.8 us)
+  const int64_t nrb = (max_l + tc::BM - 1) / tc::BM;
+  if (!wide && max_l > tc::BM && small_bns_one_wave(cols, nrb, tc::BM * tc::BK * 2) == 0)
     return false;
   return true;
 }

@@ -369,14 +369,15 @@ def test_fused_allgather_single_device_ranks(dtype, L, world, cuda):
 
 
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
-@pytest.mark.parametrize("L", [1, 7, 64, 128, 129, 200, 256])
+@pytest.mark.parametrize("L", [1, 7, 64, 128, 129, 200, 256, 300, 384, 500, 640])
 def test_small_l_kernel_bit_identical_to_persistent_kernel(dtype, L, cuda):
-    """L <= 128 runs the small-L (decode) kernel; its rows equal, bit for bit, the same
-    rows computed by the persistent kernel inside a longer batch (same FP32 tensor-core
-    accumulation, same FHADD + rounding), for both tags, grouped, and head-major."""
+    """L <= 640 at this width runs the small-L (decode) kernel (32 / 64 / 128 / 160-column
+    blocks by L); its rows equal, bit for bit, the same rows computed by the
+    persistent kernel inside a longer batch (same FP32 tensor-core accumulation, same
+    FHADD + rounding), for both tags, grouped, and head-major."""
     d, d_h, n = 512, 128, 16
     g = torch.Generator().manual_seed(L)
-    x_long = torch.randn(300, d, generator=g).to(dtype).to(cuda)
+    x_long = torch.randn(1500, d, generator=g).to(dtype).to(cuda)
     ck = (torch.randn(d - d_h, n * d_h, generator=g) / 8).to(dtype).to(cuda)
     cv = (torch.randn(d - d_h, n * d_h, generator=g) / 8).to(dtype).to(cuda)
     specs = [(ck, d_h, n, bd.Tag.FIRST), (cv, d_h, n, bd.Tag.LAST)]

@@ -67,6 +67,12 @@ def main():
             k, v = bd.fused_kv_proj_grouped(x[:L].contiguous(), [(ck, 128, 8, bd.Tag.FIRST),
                                                                  (cv, 128, 8, bd.Tag.LAST)])
             check(k, ref(x[:L], ck, 128, 8, bd.Tag.FIRST), tol)
+        # small-L kernel, 32- and 160-column blocks (4096 columns: L = 100 and L = 600)
+        cw = (torch.randn(384, 2048, generator=g) / 8).to(dt).to(dev)
+        for L in (100, 600):
+            k, v = bd.fused_kv_proj_grouped(x[:L].contiguous(), [(cw, 128, 16, bd.Tag.FIRST),
+                                                                 (cw, 128, 16, bd.Tag.LAST)])
+            check(v, ref(x[:L], cw, 128, 16, bd.Tag.LAST), tol)
         # fused RMSNorm variant
         gamma = (0.5 + torch.rand(512, generator=g)).to(dev)
         fk = bd.fold_rmsnorm(ck, gamma, 128, bd.Tag.FIRST)
